@@ -1,0 +1,214 @@
+"""Operator layer: the reference's `geofield.backend` surface, bound to CUDA.
+
+Mirrors /root/reference/pkg/src/geofield/backend.py (same function names,
+argument meaning and error behaviour) but dispatches to the sm_100a kernels
+of libgeofield_b200.so through the C ABI (include/geofield_b200.h).  There is
+exactly one backend; there is no CPU fallback (`use("fallback")` raises).
+
+Additions over the reference surface:
+  * precision control (`set_precision("fp32"|"fp64")`, env
+    GEOFIELD_PRECISION): fp32 is the product default (complex64 windows,
+    FP32 arithmetic, within 1e-4 of the float64 reference); fp64 reproduces
+    the reference's tight tolerances.
+  * DeviceWindow: a device-resident window handle; `cascade` accepts these
+    (no per-call marshalling) as well as plain numpy windows.
+  * cascade_batch: the batched pose sweep (Q3) on device arrays.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _lib
+from ._lib import LIB, check, dptr
+
+HAVE_CORE = True  # the CUDA engine is the only (and compiled) backend
+
+_NAMES = ("cuda", "core")
+_active = "cuda"
+
+_env_prec = os.environ.get("GEOFIELD_PRECISION", "fp32").strip().lower()
+if _env_prec not in ("fp32", "fp64"):
+    raise ImportError(f"GEOFIELD_PRECISION must be fp32 or fp64, got {_env_prec!r}")
+_precision = _env_prec
+
+
+def current():
+    return _active
+
+
+def use(name):
+    """Reference-compatible switch (backend.py:37-44).
+
+    "core"/"cuda" select the compiled CUDA engine; "fallback" is refused
+    because this engine deliberately has no CPU path; anything else is a
+    ValueError exactly like the reference.
+    """
+    global _active
+    if name == "fallback":
+        raise RuntimeError("the B200 engine has no CPU fallback backend")
+    if name not in _NAMES:
+        raise ValueError(f"unknown backend {name!r}")
+    _active = "cuda"
+
+
+def default_threads():
+    """Kept for API compatibility (backend.py:47-52); the GPU ignores it."""
+    try:
+        n = int(os.environ.get("GEOFIELD_THREADS", "1"))
+    except ValueError:
+        n = 1
+    return max(1, n)
+
+
+def precision():
+    return _precision
+
+
+def set_precision(name):
+    global _precision
+    if name not in ("fp32", "fp64"):
+        raise ValueError("precision must be 'fp32' or 'fp64'")
+    _precision = name
+
+
+def _prec_bits(prec=None):
+    return 64 if (prec or _precision) == "fp64" else 32
+
+
+# ---------------------------------------------------------------------------
+# device-resident windows
+
+
+class DeviceWindow:
+    """A centre-referenced window living in HBM behind a C-ABI handle.
+
+    Created from a host complex128 array or a CUDA complex128 torch tensor.
+    `np.asarray(win)` materialises the host copy (cached).
+    """
+
+    def __init__(self, data, dimension=None):
+        _lib.ensure_device()
+        self._host = None
+        h = ctypes.c_uint64(0)
+        if isinstance(data, np.ndarray):
+            arr = np.ascontiguousarray(data, dtype=np.complex128)
+            d = arr.ndim if dimension is None else dimension
+            w = (ctypes.c_int32 * 3)(*(list(arr.shape) + [1] * (3 - arr.ndim)))
+            check(LIB.gf_window_create(dptr(arr.view(np.float64)), d, w, ctypes.byref(h)))
+            self._host = arr
+            self.shape = tuple(arr.shape)
+        else:  # torch tensor on the device
+            import torch
+
+            t = data.contiguous()
+            if t.dtype != torch.complex128:
+                t = t.to(torch.complex128)
+            d = t.dim() if dimension is None else dimension
+            w = (ctypes.c_int32 * 3)(*(list(t.shape) + [1] * (3 - t.dim())))
+            st = torch.cuda.current_stream(t.device).cuda_stream
+            check(LIB.gf_window_create_device(ctypes.c_void_p(t.data_ptr()), d, w, ctypes.byref(h),
+                                              ctypes.c_void_p(st)))
+            self._dev = t
+            self.shape = tuple(t.shape)
+        self.handle = h.value
+        self.ndim = len(self.shape)
+
+    def __array__(self, dtype=None, copy=None):
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+        return self._host if dtype is None else self._host.astype(dtype)
+
+    def ravel(self):
+        return np.asarray(self).ravel()
+
+    def reshape(self, *shape):
+        return np.asarray(self).reshape(*shape)
+
+    def __getitem__(self, idx):
+        return np.asarray(self)[idx]
+
+    def __len__(self):
+        return self.shape[0]
+
+    def __del__(self):
+        h = getattr(self, "handle", 0)
+        if h:
+            try:
+                LIB.gf_window_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+
+
+def as_device_window(C):
+    return C if isinstance(C, DeviceWindow) else DeviceWindow(np.asarray(C))
+
+
+# ---------------------------------------------------------------------------
+# cascade (Q1) and batched sweep (Q3)
+
+
+def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
+    """Score + gradients over one retained-mode window (backend.py:153-164).
+
+    Returns complex128[1 + d + n_rot]: [score, dS/dt..., dS/dtheta...], times
+    dcell, computed by the CUDA cascade kernel.
+    """
+    W1, W2 = as_device_window(C1), as_device_window(C2)
+    d = W1.ndim
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    t_eff = np.ascontiguousarray(t_eff, dtype=np.float64)
+    center = np.ascontiguousarray(center, dtype=np.float64)
+    dom = np.ascontiguousarray(domega, dtype=np.float64)
+    out = np.empty(7 if d == 3 else 4, dtype=np.complex128)
+    check(LIB.gf_cascade(W1.handle, W2.handle, int(bool(wrap)), dptr(dom), float(dcell), dptr(R), dptr(t_eff),
+                         dptr(center), _prec_bits(precision), dptr(out.view(np.float64))))
+    return out
+
+
+def pack_poses(R, t_eff):
+    """(n, d, d) rotations + (n, d) effective translations -> (n, 12) float64."""
+    R = np.asarray(R, dtype=np.float64)
+    t = np.asarray(t_eff, dtype=np.float64)
+    n, d = t.shape
+    out = np.zeros((n, 12))
+    if d == 3:
+        out[:, :9] = R.reshape(n, 9)
+        out[:, 9:] = t
+    else:
+        out[:, 0], out[:, 1], out[:, 3], out[:, 4] = R[:, 0, 0], R[:, 0, 1], R[:, 1, 0], R[:, 1, 1]
+        out[:, 8] = 1.0
+        out[:, 9:11] = t
+    return out
+
+
+def cascade_batch(C1, C2, wrap, domega, dcell, center, poses, out=None, precision=None, stream=None,
+                  serial=False):
+    """Batched cascade over poses (torch CUDA float64 tensor (n, 12), see
+    pack_poses).  Returns a (n, 14) float64 CUDA tensor: interleaved complex
+    [S, Tx, Ty, Tz, Gx, Gy, Gz] (2D: the rotational term is column pair 6).
+
+    serial=True issues one single-query launch per pose (the haptic loop);
+    otherwise one launch covers all poses (the pose sweep)."""
+    import torch
+
+    W1, W2 = as_device_window(C1), as_device_window(C2)
+    if not (poses.is_cuda and poses.dtype == torch.float64 and poses.is_contiguous()):
+        raise ValueError("poses must be a contiguous float64 CUDA tensor of shape (n, 12)")
+    n = poses.shape[0]
+    if out is None:
+        out = torch.empty((n, 14), dtype=torch.float64, device=poses.device)
+    d = W1.ndim
+    dom = np.zeros(3)
+    dom[:d] = domega
+    cen = np.zeros(3)
+    cen[:d] = center
+    st = stream if stream is not None else torch.cuda.current_stream(poses.device).cuda_stream
+    fn = LIB.gf_cascade_serial if serial else LIB.gf_cascade_batch
+    check(fn(W1.handle, W2.handle, int(bool(wrap)), dptr(dom), float(dcell), dptr(cen),
+                               _prec_bits(precision), int(n), ctypes.c_void_p(poses.data_ptr()),
+                               ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st)))
+    return out

@@ -1,0 +1,333 @@
+// capi.cu -- extern "C" boundary of libgeofield_b200.so (include/geofield_b200.h).
+//
+// Owns the device-resident window table and the per-thread query contexts;
+// everything numerical lives in the kernel files.
+#include "../../include/geofield_b200.h"
+#include "cascade.cuh"
+#include "common.cuh"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+namespace gf {
+
+static thread_local std::string tl_error;
+void set_error(const std::string& msg) { tl_error = msg; }
+const char* last_error() { return tl_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// windows
+
+struct Window {
+  int device = 0;
+  int d = 3;
+  int w[3] = {1, 1, 1};
+  int64_t n = 0;
+  void* raw64 = nullptr;            // complex128
+  void* raw32 = nullptr;            // complex64 (lazy)
+  void* packed[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [prec32?0:1][wrap]
+  ~Window() {
+    cudaFree(raw64);
+    cudaFree(raw32);
+    for (auto& p : packed)
+      for (auto q : p) cudaFree(q);
+  }
+};
+
+static std::mutex g_mu;
+static std::unordered_map<uint64_t, std::unique_ptr<Window>> g_windows;
+static uint64_t g_next_handle = 1;
+
+static Window* find_window(uint64_t h) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_windows.find(h);
+  return it == g_windows.end() ? nullptr : it->second.get();
+}
+
+// ---------------------------------------------------------------------------
+// per-thread query context: high-priority stream, mapped result slot, scratch
+
+struct Context {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  double* host_out = nullptr;     // pinned + mapped, 14 doubles
+  double* dev_out_alias = nullptr;
+  double* partials = nullptr;
+  unsigned* counters = nullptr;
+  int64_t partials_cap = 0, counters_cap = 0;
+};
+static thread_local Context tl_ctx;
+static int g_run_length = 0;
+
+static int ensure_context() {
+  int dev = 0;
+  GF_CUDA(cudaGetDevice(&dev));
+  Context& c = tl_ctx;
+  if (c.device == dev && c.stream) return 0;
+  int lo = 0, hi = 0;
+  GF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  GF_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi));
+  GF_CUDA(cudaHostAlloc((void**)&c.host_out, 64 * sizeof(double), cudaHostAllocMapped));
+  GF_CUDA(cudaHostGetDevicePointer((void**)&c.dev_out_alias, c.host_out, 0));
+  c.device = dev;
+  return 0;
+}
+
+static int ensure_scratch(Context& c, int64_t n_partials, int64_t n_counters, cudaStream_t st) {
+  if (n_partials > c.partials_cap) {
+    cudaFree(c.partials);
+    c.partials = nullptr;
+    GF_CUDA(cudaMalloc((void**)&c.partials, n_partials * sizeof(double)));
+    c.partials_cap = n_partials;
+  }
+  if (n_counters > c.counters_cap) {
+    cudaFree(c.counters);
+    c.counters = nullptr;
+    GF_CUDA(cudaMalloc((void**)&c.counters, n_counters * sizeof(unsigned)));
+    GF_CUDA(cudaMemsetAsync(c.counters, 0, n_counters * sizeof(unsigned), st));
+    GF_CUDA(cudaStreamSynchronize(st));
+    c.counters_cap = n_counters;
+  }
+  return 0;
+}
+
+// raw (complex<T>) and packed moving-operand layouts, built lazily once
+static int window_raw(Window* win, int precision, cudaStream_t st, const void** out) {
+  if (precision == 64) {
+    *out = win->raw64;
+    return 0;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!win->raw32) {
+    GF_CUDA(cudaMalloc(&win->raw32, win->n * 2 * sizeof(float)));
+    GF_CUDA(launch_narrow(win->raw64, win->raw32, win->n, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+  }
+  *out = win->raw32;
+  return 0;
+}
+
+static int window_packed(Window* win, int precision, int wrap, cudaStream_t st, const void** out) {
+  const void* raw = nullptr;
+  int rc = window_raw(win, precision, st, &raw);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_mu);
+  void*& slot = win->packed[precision == 32 ? 0 : 1][wrap ? 1 : 0];
+  if (!slot) {
+    size_t elem = precision == 32 ? 4 * sizeof(float) : 4 * sizeof(double);
+    GF_CUDA(cudaMalloc(&slot, packed_window_elems(win->w) * elem));
+    GF_CUDA(launch_pack_window(precision, raw, slot, win->w, wrap, st));
+    GF_CUDA(cudaStreamSynchronize(st));
+  }
+  *out = slot;
+  return 0;
+}
+
+static int new_window(int d, const int32_t* w, Window** out, uint64_t* handle) {
+  GF_CHECK(d == 2 || d == 3, GF_EINVAL, "window dimension must be 2 or 3");
+  GF_CHECK(w != nullptr && handle != nullptr, GF_EINVAL, "null argument");
+  auto win = std::make_unique<Window>();
+  win->d = d;
+  for (int a = 0; a < 3; ++a) win->w[a] = (a < d) ? w[a] : 1;
+  for (int a = 0; a < d; ++a) GF_CHECK(win->w[a] >= 2 && win->w[a] % 2 == 0, GF_EINVAL, "window sides must be even");
+  win->n = (int64_t)win->w[0] * win->w[1] * win->w[2];
+  GF_CUDA(cudaGetDevice(&win->device));
+  GF_CUDA(cudaMalloc(&win->raw64, win->n * 2 * sizeof(double)));
+  *out = win.get();
+  std::lock_guard<std::mutex> lk(g_mu);
+  *handle = g_next_handle++;
+  g_windows[*handle] = std::move(win);
+  return 0;
+}
+
+// common argument setup for both query entry points
+static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const double* domega, double dcell,
+                     const double* center, int precision, cudaStream_t st) {
+  GF_CHECK(w1 && w2, GF_EINVAL, "unknown window handle");
+  GF_CHECK(precision == 32 || precision == 64, GF_EINVAL, "precision must be 32 or 64");
+  GF_CHECK(w1->d == w2->d, GF_EINVAL, "window dimension mismatch");
+  for (int ax = 0; ax < 3; ++ax) GF_CHECK(w1->w[ax] == w2->w[ax], GF_EINVAL, "window shape mismatch");
+  std::memset(&a, 0, sizeof a);
+  int rc = window_raw(w1, precision, st, &a.C1);
+  if (rc) return rc;
+  rc = window_packed(w2, precision, wrap, st, &a.C2p);
+  if (rc) return rc;
+  for (int ax = 0; ax < 3; ++ax) a.w[ax] = w1->w[ax];
+  a.dim = w1->d;
+  a.wrap = wrap ? 1 : 0;
+  a.precision = precision;
+  for (int ax = 0; ax < 3; ++ax) {
+    a.dom[ax] = (ax < w1->d) ? domega[ax] : 1.0;
+    a.center[ax] = (ax < w1->d) ? center[ax] : 0.0;
+  }
+  for (int ax = 0; ax < w1->d; ++ax) GF_CHECK(a.dom[ax] > 0.0, GF_EINVAL, "domega must be positive");
+  a.dcell = dcell;
+  a.seg_len = g_run_length;
+  return 0;
+}
+
+static void embed_pose(int d, const double* R, const double* t, double* dst) {
+  if (d == 3) {
+    std::memcpy(dst, R, 9 * sizeof(double));
+    std::memcpy(dst + 9, t, 3 * sizeof(double));
+  } else {
+    const double e[12] = {R[0], R[1], 0.0, R[2], R[3], 0.0, 0.0, 0.0, 1.0, t[0], t[1], 0.0};
+    std::memcpy(dst, e, sizeof e);
+  }
+}
+
+}  // namespace gf
+
+using namespace gf;
+
+extern "C" {
+
+int gf_version(void) { return 1; }
+const char* gf_last_error(void) { return gf::last_error(); }
+
+int gf_init(int device) {
+  GF_CUDA(cudaSetDevice(device));
+  return ensure_context();
+}
+
+int gf_window_create(const double* host_c128, int d, const int32_t* w, uint64_t* handle) {
+  GF_CHECK(host_c128 != nullptr, GF_EINVAL, "null window data");
+  int rc = ensure_context();
+  if (rc) return rc;
+  Window* win = nullptr;
+  rc = new_window(d, w, &win, handle);
+  if (rc) return rc;
+  GF_CUDA(cudaMemcpyAsync(win->raw64, host_c128, win->n * 2 * sizeof(double), cudaMemcpyHostToDevice,
+                          tl_ctx.stream));
+  GF_CUDA(cudaStreamSynchronize(tl_ctx.stream));
+  return 0;
+}
+
+int gf_window_create_device(const void* dev_c128, int d, const int32_t* w, uint64_t* handle, void* stream) {
+  GF_CHECK(dev_c128 != nullptr, GF_EINVAL, "null window data");
+  int rc = ensure_context();
+  if (rc) return rc;
+  Window* win = nullptr;
+  rc = new_window(d, w, &win, handle);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  GF_CUDA(cudaMemcpyAsync(win->raw64, dev_c128, win->n * 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int gf_window_destroy(uint64_t handle) {
+  std::unique_ptr<Window> victim;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_windows.find(handle);
+    GF_CHECK(it != g_windows.end(), GF_EINVAL, "unknown window handle");
+    victim = std::move(it->second);
+    g_windows.erase(it);
+  }
+  return 0;
+}
+
+int gf_window_device_ptr(uint64_t handle, const void** dev_c128) {
+  Window* w = find_window(handle);
+  GF_CHECK(w && dev_c128, GF_EINVAL, "unknown window handle");
+  *dev_c128 = w->raw64;
+  return 0;
+}
+
+int gf_set_cascade_run_length(int L) {
+  GF_CHECK(L >= 0 && L <= 1024, GF_EINVAL, "run length out of range");
+  g_run_length = L;
+  return 0;
+}
+
+int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double dcell, const double* R,
+               const double* t_eff, const double* center, int precision, double* out) {
+  GF_CHECK(domega && R && t_eff && center && out, GF_EINVAL, "null argument");
+  int rc = ensure_context();
+  if (rc) return rc;
+  Context& c = tl_ctx;
+  Window* w1 = find_window(h1);
+  Window* w2 = find_window(h2);
+  CascadeArgs a;
+  rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, c.stream);
+  if (rc) return rc;
+  embed_pose(w1->d, R, t_eff, a.pose_inline);
+  a.poses = nullptr;
+  plan_cascade(a, 1, 2 * 148);
+  rc = ensure_scratch(c, (int64_t)a.blocks_per_pose * kNumMoments, 1, c.stream);
+  if (rc) return rc;
+  a.partials = c.partials;
+  a.counters = c.counters;
+  a.out = c.dev_out_alias;
+  GF_CUDA(launch_cascade(a, 1, c.stream));
+  GF_CUDA(cudaStreamSynchronize(c.stream));
+  if (w1->d == 3) {
+    std::memcpy(out, c.host_out, 14 * sizeof(double));
+  } else {  // [S, Tx, Ty, Gz]
+    std::memcpy(out, c.host_out, 6 * sizeof(double));
+    out[6] = c.host_out[12];
+    out[7] = c.host_out[13];
+  }
+  return 0;
+}
+
+int gf_cascade_batch(uint64_t h1, uint64_t h2, int wrap, const double* domega, double dcell, const double* center,
+                     int precision, int64_t n, const double* poses_dev, double* out_dev, void* stream) {
+  GF_CHECK(domega && center && poses_dev && out_dev, GF_EINVAL, "null argument");
+  GF_CHECK(n >= 0, GF_EINVAL, "negative pose count");
+  if (n == 0) return 0;
+  int rc = ensure_context();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  Window* w1 = find_window(h1);
+  Window* w2 = find_window(h2);
+  CascadeArgs a;
+  rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, st);
+  if (rc) return rc;
+  a.poses = poses_dev;
+  plan_cascade(a, n, 4 * 148);
+  if (a.blocks_per_pose > 1) {
+    rc = ensure_scratch(tl_ctx, n * a.blocks_per_pose * kNumMoments, n, st);
+    if (rc) return rc;
+    a.partials = tl_ctx.partials;
+    a.counters = tl_ctx.counters;
+  }
+  a.out = out_dev;
+  GF_CUDA(launch_cascade(a, n, st));
+  return 0;
+}
+
+int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, double dcell, const double* center,
+                      int precision, int64_t n, const double* poses_dev, double* out_dev, void* stream) {
+  GF_CHECK(domega && center && poses_dev && out_dev, GF_EINVAL, "null argument");
+  GF_CHECK(n >= 0, GF_EINVAL, "negative pose count");
+  if (n == 0) return 0;
+  int rc = ensure_context();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  Window* w1 = find_window(h1);
+  Window* w2 = find_window(h2);
+  CascadeArgs a;
+  rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, st);
+  if (rc) return rc;
+  plan_cascade(a, 1, 2 * 148);
+  rc = ensure_scratch(tl_ctx, (int64_t)a.blocks_per_pose * kNumMoments, 1, st);
+  if (rc) return rc;
+  a.partials = tl_ctx.partials;
+  a.counters = tl_ctx.counters;
+  // one single-query launch per pose, stream-ordered (the haptic loop shape)
+  for (int64_t i = 0; i < n; ++i) {
+    a.poses = poses_dev + 12 * i;
+    a.out = out_dev + 14 * i;
+    GF_CUDA(launch_cascade(a, 1, st));
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+"""Q1 cascade kernel vs the oracle (C restatement of _core.cascade_3d/2d).
+
+Tolerances (stated): fp32 engine |new - ref| <= 1e-4 * max(|ref|, L1) with
+L1 = dcell * sum|summand| per output; fp64 engine
+<= 1e-10 relative to max(|ref|, L1) (the reference's own test_backend
+cascade tolerance, test_backend.py:79-108).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import lattice_rotations_3d, parity_tol, random_rotation, synthetic_window
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def be():
+    from paper_1711_05017_b200 import backend
+
+    return backend
+
+
+CASES = [(8, False), (16, False), (16, True), (32, False), (12, False), (10, True)]
+
+
+@pytest.mark.parametrize("w,wrap", CASES)
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_cascade_3d_generic_rotations(be, w, wrap, prec, tol):
+    rng = np.random.default_rng(1000 + w + 7 * wrap)
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom = (0.11, 0.11, 0.11)
+    dcell = 0.37
+    center = rng.normal(size=3)
+    for _ in range(4):
+        R = random_rotation(rng)
+        t = rng.uniform(-3, 3, size=3)
+        got = be.cascade(W1, W2, wrap, dom, dcell, R, t, center, precision=prec)
+        want = oracle.cascade(C1, C2, wrap, dom, dcell, R, t, center)
+        l1 = oracle.cascade_term_scales(C1, C2, wrap, dom, dcell, R, t, center)
+        assert np.all(parity_tol(got, want, l1, tol)), (got, want, l1)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_cascade_3d_lattice_rotations_torque_exact_cell(be, prec, tol):
+    """At lattice rotations the float64 floor decision must match the
+    reference so the torque takes the same trilinear cell."""
+    rng = np.random.default_rng(7)
+    w = 16
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom = (1.0 / (16 * 0.3),) * 3  # non-dyadic spacing: ties land on both sides
+    for R in lattice_rotations_3d()[::3]:
+        t = rng.uniform(-1, 1, size=3)
+        got = be.cascade(W1, W2, False, dom, 0.5, R, t, np.array([0.1, -0.2, 0.3]), precision=prec)
+        want = oracle.cascade(C1, C2, False, dom, 0.5, R, t, np.array([0.1, -0.2, 0.3]))
+        l1 = oracle.cascade_term_scales(C1, C2, False, dom, 0.5, R, t, np.array([0.1, -0.2, 0.3]))
+        assert np.all(parity_tol(got, want, l1, tol))
+
+
+def test_cascade_2d(be):
+    rng = np.random.default_rng(3)
+    for w, wrap in [(16, False), (32, True)]:
+        C1 = synthetic_window(rng, w, 2)
+        C2 = synthetic_window(rng, w, 2)
+        th = 0.37
+        R = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+        t = np.array([0.3, -0.7])
+        c = np.array([0.2, 0.1])
+        for prec, tol in [("fp32", 1e-4), ("fp64", 1e-10)]:
+            got = be.cascade(C1, C2, wrap, (0.2, 0.2), 0.3, R, t, c, precision=prec)
+            want = oracle.cascade(C1, C2, wrap, (0.2, 0.2), 0.3, R, t, c)
+            l1 = oracle.cascade_term_scales(C1, C2, wrap, (0.2, 0.2), 0.3, R, t, c)
+            assert got.shape == (4,)
+            assert np.all(parity_tol(got, want, l1, tol)), (prec, got, want)
+
+
+def test_cascade_deterministic(be):
+    rng = np.random.default_rng(11)
+    C1, C2 = synthetic_window(rng, 32), synthetic_window(rng, 32)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    R = random_rotation(rng)
+    outs = [be.cascade(W1, W2, False, (0.1,) * 3, 1.0, R, [0.1, 0.2, 0.3], [0, 0, 0]) for _ in range(5)]
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+
+
+def test_cascade_batch_matches_single(be):
+    import torch
+
+    rng = np.random.default_rng(5)
+    w = 24
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    n = 37
+    Rs = np.stack([random_rotation(rng) for _ in range(n)])
+    ts = rng.uniform(-2, 2, size=(n, 3))
+    poses = torch.from_numpy(be.pack_poses(Rs, ts)).cuda()
+    for prec in ("fp32", "fp64"):
+        out = be.cascade_batch(W1, W2, False, (0.1,) * 3, 0.5, [0.1, 0.2, 0.3], poses, precision=prec)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.complex128)
+        for i in range(0, n, 6):
+            want = oracle.cascade(C1, C2, False, (0.1,) * 3, 0.5, Rs[i], ts[i], np.array([0.1, 0.2, 0.3]))
+            l1 = oracle.cascade_term_scales(C1, C2, False, (0.1,) * 3, 0.5, Rs[i], ts[i], np.array([0.1, 0.2, 0.3]))
+            assert np.all(parity_tol(got[i], want, l1, 1e-4 if prec == "fp32" else 1e-10))
