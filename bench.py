@@ -1,0 +1,412 @@
+"""Headline benchmark: the haptic single-query loop (BASELINE.json configs[1]).
+
+Workload (N=1): "low-clearance peg-in-hole 128^3, K=32, single-query haptic
+latency loop on 1 B200": a 128^3 grid, truncation K=32 (window side w=2K=64,
+m'=262,144 retained modes), energy + force + torque per query.  One step =
+one 1,000-query segment of a jittered insertion trajectory (R near I,
+sigma_theta = 0.5 deg; t sliding along z with sigma_t = h/4), issued as
+1,000 serial single-query launches.
+
+  value   queries/s of the device-resident loop (windows and poses already in
+          HBM; one kernel launch per query, stream-ordered), CUDA events.
+  e2e     queries/s through the reference-facing operator call
+          (backend.cascade: host pose in, host complex128[7] out, the
+          per-query H2D/D2H inside the timed region), with p50/p95/p99 per
+          query as cmd_bench defines them (cli.py:357-361).
+  roofline  the cascade kernel against the FP32 FMA pipe measured live on
+          this GPU (MEASURED_PEAKS.json has no FP32 figure); algorithmic work
+          240 FP32 flops per live retained mode.
+  cpu_baseline  the reference's own compiled kernel (_core.cascade_3d built
+          from /root/reference into oracle/_ref) on the same windows, 1 core
+          (it is single-threaded by design, backend.py:153-164).
+
+--impl reference runs the reference kernel with every host core (a thread
+pool over poses; _core.cascade_3d releases the GIL) on the same config.
+
+Multi-GPU: the single haptic query does not shard:
+`--gpus N` runs N independent replicas, one per rank, and value/e2e are the
+whole-job totals (max-over-ranks time).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GRID_N = 128
+K_TRUNC = 32
+W = 2 * K_TRUNC
+DOMAIN = 3.46  # grid_for_pair domain of the C1/C2 peg pair
+QUERIES_PER_STEP = 1000
+SEED = 20260814
+
+
+def synthetic_windows(w, seed=SEED):
+    """CN(0,1)(1+|k|^2)^-1 windows (SURVEY.md 8(d) micro-benchmark law)."""
+    rng = np.random.default_rng(seed)
+    k = np.stack(np.meshgrid(*[np.arange(w) - w // 2] * 3, indexing="ij"), axis=-1)
+    amp = 1.0 / (1.0 + np.sum(k * k, axis=-1))
+    C1 = (rng.normal(size=(w,) * 3) + 1j * rng.normal(size=(w,) * 3)) * amp
+    C2 = (rng.normal(size=(w,) * 3) + 1j * rng.normal(size=(w,) * 3)) * amp
+    return C1, C2
+
+
+def grid_params():
+    h = DOMAIN / GRID_N
+    origin = -0.5 * DOMAIN
+    center = np.full(3, origin + h * (GRID_N // 2))
+    dom = np.full(3, 1.0 / (GRID_N * h))
+    dcell = 1.0 / (GRID_N ** 3 * h ** 3)
+    return h, center, dom, dcell
+
+
+def axis_rot(axis, ang):
+    c, s = np.cos(ang), np.sin(ang)
+    R = np.eye(3)
+    i, j = [(1, 2), (0, 2), (0, 1)][axis]
+    R[i, i], R[i, j], R[j, i], R[j, j] = c, -s, s, c
+    return R
+
+
+def trajectory(n, seed):
+    """Jittered insertion path: R ~ I (0.5 deg jitter), t_z from 0.4 to 0."""
+    h, center, _, _ = grid_params()
+    rng = np.random.default_rng(seed)
+    s = np.linspace(0.0, 1.0, n)
+    Rs, ts = [], []
+    for k in range(n):
+        j = np.deg2rad(0.5) * rng.normal(size=3)
+        R = axis_rot(0, j[0]) @ axis_rot(1, j[1]) @ axis_rot(2, j[2])
+        t = np.array([0.0, 0.0, 0.4 * (1.0 - s[k])]) + (h / 4) * rng.normal(size=3)
+        Rs.append(R)
+        ts.append(t)
+    Rs, ts = np.asarray(Rs), np.asarray(ts)
+    t_eff = ts - center + Rs @ center  # energy.py:177
+    return Rs, ts, t_eff
+
+
+def live_fraction(Rs, w, sample=8):
+    """Share of retained modes whose trilinear footprint touches the window
+    (the rest contribute exact zeros), averaged over a few poses."""
+    k = np.stack(np.meshgrid(*[np.arange(w) - w // 2] * 3, indexing="ij"), axis=-1).reshape(-1, 3)
+    fr = []
+    for R in Rs[:: max(1, len(Rs) // sample)][:sample]:
+        u = -(k @ R) + w // 2
+        fl = np.floor(u)
+        ok = np.all((fl >= -1) & (fl <= w - 1), axis=1)
+        fr.append(ok.mean())
+    return float(np.mean(fr))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (the reference's compiled kernel, oracle/_ref)
+
+
+def reference_core():
+    import oracle
+
+    core = oracle.ref_core()
+    if core is None:
+        raise RuntimeError("oracle/_ref not built (make -C oracle ref in the build container)")
+    return core
+
+
+def cpu_reference_rate(C1, C2, Rs, t_eff, threads, budget_s):
+    """Queries/s of _core.cascade_3d on `threads` host threads for ~budget_s."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    core = reference_core()
+    _, center, dom, dcell = grid_params()
+    C1 = np.ascontiguousarray(C1)
+    C2 = np.ascontiguousarray(C2)
+
+    def one(i):
+        return core.cascade_3d(C1, C2, False, dom[0], dom[1], dom[2], dcell, np.ascontiguousarray(Rs[i]),
+                               np.ascontiguousarray(t_eff[i]), center)
+
+    one(0)  # warm
+    t0 = time.perf_counter()
+    one(1)
+    per = time.perf_counter() - t0
+    n = max(threads, int(budget_s * threads / max(per, 1e-6)))
+    n = min(n, len(Rs))
+    t0 = time.perf_counter()
+    if threads == 1:
+        for i in range(n):
+            one(i)
+    else:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            list(pool.map(one, range(n)))
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def run_reference_arm(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    C1, C2 = synthetic_windows(W)
+    Rs, _, t_eff = trajectory(max(4096, QUERIES_PER_STEP), SEED)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_rate(C1, C2, Rs, t_eff, threads, 0.5)
+    rates, samples = [], []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        r, n, dt = cpu_reference_rate(C1, C2, Rs, t_eff, threads, args.ref_seconds)
+        rates.append(r)
+        samples.append(n)
+    total = time.perf_counter() - t_all
+    value = float(np.sum(samples) / total)
+    line = {
+        "impl": "reference", "metric": "pose queries/sec (energy+force+torque) at K=32, 128^3, single-query loop",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 haptic query loop: 128^3 grid, K=32 (w=64, m'=262144)",
+                   "grid": GRID_N, "K": K_TRUNC, "w": W, "m_prime": W ** 3},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "reference",
+                         "sample": f"{int(np.mean(samples))} poses of the trajectory per step, "
+                                   f"_core.cascade_3d on a {threads}-thread pool"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# engine arm
+
+
+def run_engine(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    from paper_1711_05017_b200 import _lib, backend
+
+    _lib.ensure_device(local)
+    prec = args.precision
+    h, center, dom, dcell = grid_params()
+    C1, C2 = synthetic_windows(W)
+    W1, W2 = backend.DeviceWindow(C1), backend.DeviceWindow(C2)
+    n_total = QUERIES_PER_STEP * (args.steps + args.warmup)
+    Rs, ts, t_eff = trajectory(n_total, SEED + rank)
+    poses = torch.from_numpy(backend.pack_poses(Rs, t_eff)).cuda()
+    out = torch.empty((n_total, 14), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(int(256 * 2 ** 20) // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    def step(i):
+        sl = slice(i * QUERIES_PER_STEP, (i + 1) * QUERIES_PER_STEP)
+        backend.cascade_batch(W1, W2, False, dom, dcell, center, poses[sl], out=out[sl], precision=prec,
+                              serial=True)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region: K steps, per-step events, L2 flushed between steps
+    barrier(world)
+    torch.cuda.synchronize()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(args.warmup + k)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    barrier(world)
+    local_total_ms = float(np.sum(step_ms))
+    total_ms = max_over_ranks(local_total_ms, world)
+    queries = QUERIES_PER_STEP * args.steps * world
+    value = queries / (total_ms * 1e-3)
+    kernel_us = 1e3 * local_total_ms / (QUERIES_PER_STEP * args.steps)
+
+    # ---- e2e through the operator call with host buffers
+    Re, _, te = trajectory(args.e2e_queries + 50, SEED + 7 + rank)
+    lat = []
+    for i in range(50):
+        backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision=prec)
+    barrier(world)
+    t0 = time.perf_counter()
+    for i in range(50, 50 + args.e2e_queries):
+        q0 = time.perf_counter_ns()
+        backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision=prec)
+        lat.append((time.perf_counter_ns() - q0) / 1e3)
+    e2e_local = time.perf_counter() - t0
+    barrier(world)
+    e2e_s = max_over_ranks(e2e_local, world)
+    e2e_value = args.e2e_queries * world / e2e_s
+    lat.sort()
+
+    def pct(p):
+        return lat[min(len(lat) - 1, int(p * len(lat)))]
+
+    # ---- roofline: cascade kernel vs the FP32 FMA pipe measured here
+    import ctypes
+
+    peak = ctypes.c_double(0.0)
+    _lib.check(_lib.LIB.gf_measure_fma_peak(64 if prec == "fp64" else 32, ctypes.byref(peak)))
+    live = live_fraction(Rs, W)
+    flops = 240.0 * live * W ** 3
+    achieved = flops / (kernel_us * 1e-6) / 1e12
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rate, n, dt = cpu_reference_rate(C1, C2, Rs, t_eff, 1, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "queries/s", "cores": 1, "kind": "reference",
+               "sample": f"{n} trajectory poses through _core.cascade_3d (oracle/_ref, built from the "
+                         f"reference sources), single thread, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "pose queries/sec (energy+force+torque) at K=32, 128^3, single-query loop",
+            "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": "C2 haptic query loop: 128^3 grid, K=32 (w=64, m'=262144), "
+                                   "1000 serial single-query launches per step",
+                       "grid": GRID_N, "K": K_TRUNC, "w": W, "m_prime": W ** 3,
+                       "queries_per_step": QUERIES_PER_STEP, "parallelism": f"replicas x{world}",
+                       "l2": "flushed between steps (256 MiB write); windows L2-resident within a step "
+                             "as in a live haptic loop"},
+            "latency_us": {"kernel_mean": kernel_us, "e2e_p50": statistics.median(lat), "e2e_p95": pct(0.95),
+                           "e2e_p99": pct(0.99), "definition": "cli.py:357-361"},
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": QUERIES_PER_STEP * 12 * 8,
+                    "d2h_bytes_per_step": QUERIES_PER_STEP * 14 * 8,
+                    "path": "backend.cascade host pose -> host complex128[7], per query"},
+            "roofline": {"bound": "fp32" if prec == "fp32" else "fp64", "achieved": achieved,
+                         "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value,
+                         "traffic": None,
+                         "work": f"240 flops x live modes ({live:.3f} x {W ** 3}) per launch",
+                         "peak_source": "FMA-chain kernel measured in this run (gf_measure_fma_peak)"},
+            "cpu_baseline": cpu,
+            "gpu_launches": QUERIES_PER_STEP * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--e2e-queries", type=int, default=2000)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=6.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

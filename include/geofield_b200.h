@@ -77,7 +77,16 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double *domega, 
                       const double *center, int precision, int64_t n, const double *poses_dev, double *out_dev,
                       void *stream);
 
-/* Tuning knob for experiments: run length along kz per thread (0 = auto). */
+/* Diagnostics: FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured with an
+ * FMA-chain kernel on the current device; the roofline denominator of the
+ * query/sweep kernels (precision 32 or 64). */
+int gf_measure_fma_peak(int precision, double *tflops);
+
+/* Tuning knobs for experiments: kernel variant (0 = u-space tiled, the
+ * default; 1 = direct gather) and the direct variant's run length along kz
+ * per thread (0 = auto). */
+int gf_set_cascade_variant(int variant);
+int gf_set_cascade_tile(int tile);
 int gf_set_cascade_run_length(int L);
 
 #ifdef __cplusplus

@@ -35,6 +35,9 @@ SIGNATURES = {
                                         c_dp, ctypes.c_int, ctypes.c_int64, c_vp, c_vp, c_vp]),
     "gf_cascade_serial": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double,
                                          c_dp, ctypes.c_int, ctypes.c_int64, c_vp, c_vp, c_vp]),
+    "gf_measure_fma_peak": (ctypes.c_int, [ctypes.c_int, c_dp]),
+    "gf_set_cascade_variant": (ctypes.c_int, [ctypes.c_int]),
+    "gf_set_cascade_tile": (ctypes.c_int, [ctypes.c_int]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),
 }
 

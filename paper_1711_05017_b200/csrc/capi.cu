@@ -63,6 +63,8 @@ struct Context {
 };
 static thread_local Context tl_ctx;
 static int g_run_length = 0;
+static int g_variant = 1;
+static int g_tile = 0;
 
 static int ensure_context() {
   int dev = 0;
@@ -155,7 +157,8 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
   std::memset(&a, 0, sizeof a);
   int rc = window_raw(w1, precision, st, &a.C1);
   if (rc) return rc;
-  rc = window_packed(w2, precision, wrap, st, &a.C2p);
+  if (g_variant == 0) rc = window_raw(w2, precision, st, &a.C2p);
+  else rc = window_packed(w2, precision, wrap, st, &a.C2p);
   if (rc) return rc;
   for (int ax = 0; ax < 3; ++ax) a.w[ax] = w1->w[ax];
   a.dim = w1->d;
@@ -168,6 +171,8 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
   for (int ax = 0; ax < w1->d; ++ax) GF_CHECK(a.dom[ax] > 0.0, GF_EINVAL, "domega must be positive");
   a.dcell = dcell;
   a.seg_len = g_run_length;
+  a.variant = g_variant;
+  a.tile_force = g_tile;
   return 0;
 }
 
@@ -237,6 +242,18 @@ int gf_window_device_ptr(uint64_t handle, const void** dev_c128) {
   Window* w = find_window(handle);
   GF_CHECK(w && dev_c128, GF_EINVAL, "unknown window handle");
   *dev_c128 = w->raw64;
+  return 0;
+}
+
+int gf_set_cascade_variant(int v) {
+  GF_CHECK(v == 0 || v == 1, GF_EINVAL, "variant must be 0 (tiled) or 1 (direct)");
+  g_variant = v;
+  return 0;
+}
+
+int gf_set_cascade_tile(int ts) {
+  GF_CHECK(ts == 0 || ts == 8 || ts == 16, GF_EINVAL, "tile must be 0 (auto), 8 or 16");
+  g_tile = ts;
   return 0;
 }
 

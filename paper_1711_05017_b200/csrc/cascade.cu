@@ -83,38 +83,11 @@ __device__ __forceinline__ double exact_u(const PoseShared& ps, const double* do
   return __dadd_rn(__ddiv_rn(-s, dom[a]), (double)ha);
 }
 
-template <typename T> struct Acc {
-  cx<T> S;       // sum bV
-  cx<T> Z[3];    // sum bV kappa_a
-  cx<T> Y[3][3]; // sum b dV_b kappa_a   (index [b][a])
-};
-
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   return v;
-}
-
-// Reduce the 26 moments across the block in a fixed order; result (float64)
-// lands in red[0..25] (shared) for thread 0's block.
-template <typename T>
-__device__ __forceinline__ void block_reduce(const Acc<T>& acc, double (*wsum)[kNumMoments], double* red) {
-  const T* v = reinterpret_cast<const T*>(&acc);
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int c = 0; c < kNumMoments; ++c) {
-    T s = warp_sum(v[c]);
-    if (lane == 0) wsum[warp][c] = (double)s;
-  }
-  __syncthreads();
-  if (threadIdx.x < kNumMoments) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += wsum[w][threadIdx.x];
-    red[threadIdx.x] = s;
-  }
-  __syncthreads();
 }
 
 // Form the seven outputs from the moments (float64), times dcell.
@@ -158,10 +131,23 @@ __device__ void finalize(const CascadeArgs& a, const PoseShared& ps, const doubl
   }
 }
 
-template <typename T>
+// Direct-gather kernel.  Lane layout: each warp owns a 4 x 8 patch of modes
+// in the (p, q) mode plane and every lane walks a run of L modes along the
+// third axis r.  Per pose, r is the mode axis whose rotated image has the
+// smallest C2-z component, i.e. the patch plane is the one whose image lies
+// closest to C2's z lines: the 32 lanes' corner pairs then share far fewer
+// 128-byte lines per load (one L1 wavefront per distinct line).
+struct Orient {
+  int p, q, r;        // mode axes: 4-lane, 8-lane, run
+  int nP, nQ, nR;     // patch tiles (16 wide) along p, q and runs along r
+  double step_re[3], step_im[3];
+};
+
+template <typename T, bool WRAP>
 __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
   using P4 = typename pair4<T>::type;
   __shared__ PoseShared ps;
+  __shared__ Orient orient;
   __shared__ double wsum[kWarps][kNumMoments];
   __shared__ double red[kNumMoments];
   __shared__ unsigned ticket;
@@ -169,73 +155,106 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
   const int bpp = a.blocks_per_pose;
   const int64_t pose = a.pose_offset + blockIdx.x / bpp;
   const int blk = blockIdx.x % bpp;
+  const int tid = threadIdx.x;
+  const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
+  const int L = a.seg_len;
 
-  if (threadIdx.x < 32) load_pose(a, pose, ps);
+  if (tid < 32) load_pose(a, pose, ps);
+  __syncthreads();
+  if (tid == 0) {
+    // run axis r: smallest |R[b][2]| (equal spacing: C2-z component of mode axis b)
+    int r = 2;
+    if (a.dim == 3) {
+      double z[3] = {fabs(ps.mu[2][0]), fabs(ps.mu[2][1]), fabs(ps.mu[2][2])};
+      r = (z[0] <= z[1] && z[0] <= z[2]) ? 0 : (z[1] <= z[2] ? 1 : 2);
+    }
+    int o1 = (r + 1) % 3, o2 = (r + 2) % 3;
+    if (a.dim == 2) { o1 = 0; o2 = 1; }
+    // the 8-lane axis q is the one whose image is most aligned with C2-z
+    bool swap = fabs(ps.mu[2][o1]) > fabs(ps.mu[2][o2]);
+    orient.p = swap ? o2 : o1;
+    orient.q = swap ? o1 : o2;
+    orient.r = r;
+    const int wv[3] = {w0, w1, w2};
+    orient.nP = (wv[orient.p] + 15) / 16;
+    orient.nQ = (wv[orient.q] + 15) / 16;
+    orient.nR = (wv[r] + L - 1) / L;
+    for (int ax = 0; ax < 3; ++ax) {
+      double s, c;
+      double t = ps.targ[ax];
+      sincospi(2.0 * (t - rint(t)), &s, &c);
+      orient.step_re[ax] = c;
+      orient.step_im[ax] = s;
+    }
+  }
   __syncthreads();
 
-  const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
-  const int L = a.seg_len;
-  const int spr = a.segs_per_row;
   const int64_t sy = (int64_t)(w2 + 1), sx = (int64_t)(w1 + 2) * (w2 + 1);
   const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
   const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
   const T eps = (T)a.tie_eps;
-  const T mz0 = (T)ps.mu[0][2], mz1 = (T)ps.mu[1][2], mz2 = (T)ps.mu[2][2];
-  const cx<T> step = mk<T>((T)ps.step_re, (T)ps.step_im);
+  const int p = orient.p, q = orient.q, r = orient.r;
+  const int wp = p == 0 ? w0 : (p == 1 ? w1 : w2);
+  const int wq = q == 0 ? w0 : (q == 1 ? w1 : w2);
+  const int wr = r == 0 ? w0 : (r == 1 ? w1 : w2);
+  const int sr = r == 0 ? w1 * w2 : (r == 1 ? w2 : 1);
+  const T mr0 = (T)ps.mu[0][r], mr1 = (T)ps.mu[1][r], mr2 = (T)ps.mu[2][r];
+  const cx<T> step = mk<T>((T)orient.step_re[r], (T)orient.step_im[r]);
+  const T er0 = r == 0 ? (T)1 : (T)0, er1 = r == 1 ? (T)1 : (T)0, er2 = r == 2 ? (T)1 : (T)0;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int dp = 4 * (warp & 3) + (lane & 3);
+  const int dq = 8 * (warp >> 2) + (lane >> 2);
+  const int units = orient.nP * orient.nQ * orient.nR;
 
-  Acc<T> acc;
-  {
-    T* v = reinterpret_cast<T*>(&acc);
-#pragma unroll
-    for (int c = 0; c < kNumMoments; ++c) v[c] = (T)0;
-  }
+  Acc26<T> acc;
+  acc.zero();
 
-  const int64_t seg_begin = (int64_t)blk * a.segs_per_block;
-  int64_t seg_end = seg_begin + a.segs_per_block;
-  if (seg_end > a.n_seg) seg_end = a.n_seg;
-
-  for (int64_t s = seg_begin + threadIdx.x; s < seg_end; s += kThreads) {
-    const int row = (int)(s / spr);
-    const int kz0 = (int)(s - (int64_t)row * spr) * L;
-    const int kx = row / w1, ky = row - (row / w1) * w1;
-    const int kend = min(kz0 + L, w2);
-    const double kapx = kx - hx, kapy = ky - hy, kapz0 = kz0 - hz;
-    // run start: continuous indices (float64 -> T) and phase seed
-    const T u0x = (T)(hx + ps.mu[0][0] * kapx + ps.mu[0][1] * kapy + ps.mu[0][2] * kapz0);
-    const T u0y = (T)(hy + ps.mu[1][0] * kapx + ps.mu[1][1] * kapy + ps.mu[1][2] * kapz0);
-    const T u0z = (T)(hz + ps.mu[2][0] * kapx + ps.mu[2][1] * kapy + ps.mu[2][2] * kapz0);
+  for (int unit = blk; unit < units; unit += bpp) {
+    const int ir = unit % orient.nR;
+    const int iq = (unit / orient.nR) % orient.nQ;
+    const int ip = unit / (orient.nR * orient.nQ);
+    const int kp = 16 * ip + dp, kq = 16 * iq + dq, kr0 = L * ir;
+    if (kp >= wp || kq >= wq) continue;
+    const int kend = min(kr0 + L, wr);
+    const int kx = p == 0 ? kp : (q == 0 ? kq : kr0);
+    const int ky = p == 1 ? kp : (q == 1 ? kq : kr0);
+    const int kz0 = p == 2 ? kp : (q == 2 ? kq : kr0);
+    const double kap[3] = {(double)(kx - hx), (double)(ky - hy), (double)(kz0 - hz)};
+    const T u0x = (T)(hx + ps.mu[0][0] * kap[0] + ps.mu[0][1] * kap[1] + ps.mu[0][2] * kap[2]);
+    const T u0y = (T)(hy + ps.mu[1][0] * kap[0] + ps.mu[1][1] * kap[1] + ps.mu[1][2] * kap[2]);
+    const T u0z = (T)(hz + ps.mu[2][0] * kap[0] + ps.mu[2][1] * kap[1] + ps.mu[2][2] * kap[2]);
     cx<T> ph;
     {
-      double cyc = ps.targ[0] * kapx + ps.targ[1] * kapy + ps.targ[2] * kapz0;
+      double cyc = ps.targ[0] * kap[0] + ps.targ[1] * kap[1] + ps.targ[2] * kap[2];
       cyc -= rint(cyc);
       T sn, cs;
       if constexpr (sizeof(T) == 4) sincospif(2.0f * (float)cyc, &sn, &cs);
       else sincospi(2.0 * cyc, &sn, &cs);
       ph = mk<T>(cs, sn);
     }
-    // per-run partial moments (kappa_x, kappa_y are constant along the run)
-    cx<T> rS = mk<T>(0, 0), rZz = mk<T>(0, 0);
+    cx<T> rS = mk<T>(0, 0), rJ = mk<T>(0, 0);
     cx<T> rX[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
-    cx<T> rXz[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
-    const cx<T>* c1row = C1 + ((int64_t)kx * w1 + ky) * w2;
+    cx<T> rXJ[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
+    int c1off = (kx * w1 + ky) * w2 + kz0;
 
-    for (int kz = kz0; kz < kend; ++kz) {
-      const T j = (T)(kz - kz0);
-      T u[3] = {fma(j, mz0, u0x), fma(j, mz1, u0y), fma(j, mz2, u0z)};
+    for (int kr = kr0; kr < kend; ++kr, c1off += sr) {
+      const T j = (T)(kr - kr0);
+      T u[3] = {fma(j, mr0, u0x), fma(j, mr1, u0y), fma(j, mr2, u0z)};
       T fl[3], f[3];
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         fl[ax] = floor(u[ax]);
         f[ax] = u[ax] - fl[ax];
       }
-      // near an integer: take the reference's float64 floor decision
       const bool tz = a.dim == 3 && (f[2] < eps || f[2] > (T)1 - eps);
       if (f[0] < eps || f[0] > (T)1 - eps || f[1] < eps || f[1] > (T)1 - eps || tz) {
+        // reference float64 floor decision for near-integer indices
+        const int kkx = r == 0 ? kr : kx, kky = r == 1 ? kr : ky, kkz = r == 2 ? kr : kz0;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
           if ((ax < 2 || tz) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
-            double ue = exact_u(ps, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+            double ue = exact_u(ps, a.dom, ax, kkx, kky, kkz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
             double fe = floor(ue);
             fl[ax] = (T)fe;
             f[ax] = (T)(ue - fe);
@@ -245,23 +264,22 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
       const cx<T> phk = ph;
       ph = ph * step;
       int ix = (int)fl[0], iy = (int)fl[1], iz = (int)fl[2];
-      if (a.wrap) {
+      if (WRAP) {
         ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
         iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
         iz = iz < 0 ? iz + w2 : (iz >= w2 ? iz - w2 : iz);
-      } else if (ix < -1 || ix > w0 - 1 || iy < -1 || iy > w1 - 1 || iz < -1 || iz > w2 - 1) {
+      } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
+                 (unsigned)(iz + 1) > (unsigned)w2) {
         continue;  // whole footprint outside the window: exact zero contribution
       }
-      const cx<T> base = c1row[kz] * phk;
-      const P4* p = C2 + (int64_t)(ix + 1) * sx + (int64_t)(iy + 1) * sy + (iz + 1);
-      P4 e00 = ldg_pair(p), e10 = ldg_pair(p + sx), e01 = ldg_pair(p + sy), e11 = ldg_pair(p + sx + sy);
-      // corners c[x][y][z]: e{x}{y} = (c[x][y][0], c[x][y][1])
+      const cx<T> base = C1[c1off] * phk;
+      const P4* ptr = C2 + ((ix + 1) * (int)sx + (iy + 1) * (int)sy + (iz + 1));
+      P4 e00 = ldg_pair(ptr), e10 = ldg_pair(ptr + sx), e01 = ldg_pair(ptr + sy), e11 = ldg_pair(ptr + sx + sy);
       const T fu = f[0], fv = f[1], fs = f[2];
       cx<T> c000 = mk<T>(e00.x, e00.y), c001 = mk<T>(e00.z, e00.w);
       cx<T> c100 = mk<T>(e10.x, e10.y), c101 = mk<T>(e10.z, e10.w);
       cx<T> c010 = mk<T>(e01.x, e01.y), c011 = mk<T>(e01.z, e01.w);
       cx<T> c110 = mk<T>(e11.x, e11.y), c111 = mk<T>(e11.z, e11.w);
-      // along x: a_yz, d_yz = c1yz - c0yz
       cx<T> d00 = c100 - c000, d01 = c101 - c001, d10 = c110 - c010, d11 = c111 - c011;
       cx<T> a00 = mk<T>(fma(fu, d00.re, c000.re), fma(fu, d00.im, c000.im));
       cx<T> a01 = mk<T>(fma(fu, d01.re, c001.re), fma(fu, d01.im, c001.im));
@@ -274,53 +292,67 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
       cx<T> dS = b1 - b0;
       cx<T> bV = base * V;
       cx<T> X0 = base * dU, X1 = base * dV, X2 = base * dS;
-      const T kz_k = (T)(kz - hz);
       rS += bV;
-      axpy(rZz, kz_k, bV);
+      axpy(rJ, j, bV);
       rX[0] += X0; rX[1] += X1; rX[2] += X2;
-      axpy(rXz[0], kz_k, X0); axpy(rXz[1], kz_k, X1); axpy(rXz[2], kz_k, X2);
+      axpy(rXJ[0], j, X0); axpy(rXJ[1], j, X1); axpy(rXJ[2], j, X2);
     }
-    const T kxk = (T)kapx, kyk = (T)kapy;
-    acc.S += rS;
-    axpy(acc.Z[0], kxk, rS);
-    axpy(acc.Z[1], kyk, rS);
-    acc.Z[2] += rZz;
+    // fold the run: sum_j kappa_a(j) Y = kappa0_a sum Y + e_r,a sum j Y
+    const T k0x = (T)kap[0], k0y = (T)kap[1], k0z = (T)kap[2];
+    T* v = acc.v;
+    v[0] += rS.re; v[1] += rS.im;
+    v[2] += k0x * rS.re + er0 * rJ.re; v[3] += k0x * rS.im + er0 * rJ.im;
+    v[4] += k0y * rS.re + er1 * rJ.re; v[5] += k0y * rS.im + er1 * rJ.im;
+    v[6] += k0z * rS.re + er2 * rJ.re; v[7] += k0z * rS.im + er2 * rJ.im;
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      axpy(acc.Y[b][0], kxk, rX[b]);
-      axpy(acc.Y[b][1], kyk, rX[b]);
-      acc.Y[b][2] += rXz[b];
+      v[8 + 6 * b] += k0x * rX[b].re + er0 * rXJ[b].re;  v[9 + 6 * b] += k0x * rX[b].im + er0 * rXJ[b].im;
+      v[10 + 6 * b] += k0y * rX[b].re + er1 * rXJ[b].re; v[11 + 6 * b] += k0y * rX[b].im + er1 * rXJ[b].im;
+      v[12 + 6 * b] += k0z * rX[b].re + er2 * rXJ[b].re; v[13 + 6 * b] += k0z * rX[b].im + er2 * rXJ[b].im;
     }
   }
 
-  block_reduce<T>(acc, wsum, red);
+  {
+    const T* v = acc.v;
+#pragma unroll
+    for (int c = 0; c < kNumMoments; ++c) {
+      T s = warp_sum(v[c]);
+      if (lane == 0) wsum[warp][c] = (double)s;
+    }
+    __syncthreads();
+    if (tid < kNumMoments) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) s += wsum[w][tid];
+      red[tid] = s;
+    }
+    __syncthreads();
+  }
 
   double* out = a.out + pose * 14;
   if (bpp == 1) {
     finalize(a, ps, red, out);
     return;
   }
-  // cross-block: publish this block's moments, last block reduces in fixed order
   double* part = a.partials + (pose * bpp + blk) * kNumMoments;
-  if (threadIdx.x < kNumMoments) part[threadIdx.x] = red[threadIdx.x];
+  if (tid < kNumMoments) part[tid] = red[tid];
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) ticket = atomicAdd(a.counters + pose, 1u);
+  if (tid == 0) ticket = atomicAdd(a.counters + pose, 1u);
   __syncthreads();
   if (ticket != (unsigned)(bpp - 1)) return;
   __threadfence();
-  const double* base = a.partials + pose * bpp * kNumMoments;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* pb = a.partials + pose * bpp * kNumMoments;
   for (int c = warp; c < kNumMoments; c += kWarps) {
     double s = 0.0;
-    for (int b = lane; b < bpp; b += 32) s += __ldcg(base + (int64_t)b * kNumMoments + c);
+    for (int b = lane; b < bpp; b += 32) s += __ldcg(pb + (int64_t)b * kNumMoments + c);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if (lane == 0) red[c] = s;
   }
   __syncthreads();
   finalize(a, ps, red, out);
-  if (threadIdx.x == 0) a.counters[pose] = 0u;  // re-arm for the next launch
+  if (tid == 0) a.counters[pose] = 0u;  // re-arm for the next launch
 }
 
 // Build the padded + z-pair-packed copy of a window for use as the moving
@@ -381,20 +413,6 @@ cudaError_t launch_narrow(const void* src, void* dst, int64_t n, cudaStream_t st
 }
 
 void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
-  // run length: L modes along kz per thread (divides work evenly when possible)
-  int w2 = a.w[2];
-  int L = a.seg_len > 0 ? a.seg_len : 8;
-  if (L > w2) L = w2;
-  a.seg_len = L;
-  a.segs_per_row = (int)ceil_div(w2, L);
-  a.n_seg = (int64_t)a.w[0] * a.w[1] * a.segs_per_row;
-  int64_t max_bpp = ceil_div(a.n_seg, kThreads);
-  int64_t bpp = 1;
-  if (n_poses < target_blocks) bpp = ceil_div(target_blocks, n_poses);
-  if (bpp > max_bpp) bpp = max_bpp;
-  if (bpp < 1) bpp = 1;
-  a.blocks_per_pose = (int)bpp;
-  a.segs_per_block = ceil_div(a.n_seg, bpp);
   // tie zone: several ulps of the largest |u| reachable at this geometry
   double umax = 0.0;
   for (int ax = 0; ax < 3; ++ax) {
@@ -406,9 +424,46 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
   double eps = 8.0 * ulp;
   double floor_eps = (a.precision == 32) ? 1e-4 : 1e-9;
   a.tie_eps = eps > floor_eps ? eps : floor_eps;
+
+  if (a.variant == 0) {
+    // u-space tiles: small tiles for a lone query (latency), large for sweeps
+    a.tile = (a.precision == 32 && n_poses >= target_blocks / 2) ? 16 : 8;
+    if (a.tile_force && (a.precision == 32 || a.tile_force == 8)) a.tile = a.tile_force;
+    int tiles = tiled_tile_count(a, a.tile);
+    int64_t bpp = 1;
+    if (n_poses < target_blocks) bpp = ceil_div(target_blocks, n_poses);
+    if (bpp > tiles) bpp = tiles;
+    a.blocks_per_pose = (int)bpp;
+    a.smem_bytes = (int)tiled_smem_bytes(a.precision, a.tile, a.w);
+    return;
+  }
+  // direct gather: 16 x 16 mode patches x runs of L along the run axis
+  int L = a.seg_len > 0 ? a.seg_len : (n_poses >= target_blocks / 2 ? 8 : 4);
+  int wmax = a.w[0] > a.w[1] ? a.w[0] : a.w[1];
+  if (a.w[2] > wmax) wmax = a.w[2];
+  if (a.dim == 2) L = 1;
+  if (L > wmax) L = wmax;
+  a.seg_len = L;
+  // units per pose depend on the pose's run axis; bound by the worst case
+  int64_t units = 1;
+  {
+    int64_t best = 0;
+    for (int r = 0; r < 3; ++r) {
+      int o1 = (r + 1) % 3, o2 = (r + 2) % 3;
+      int64_t u = ceil_div(a.w[o1], 16) * ceil_div(a.w[o2], 16) * ceil_div(a.w[r], L);
+      if (best == 0 || u < best) best = u;
+    }
+    units = best;
+  }
+  int64_t bpp = 1;
+  if (n_poses < target_blocks) bpp = ceil_div(target_blocks, n_poses);
+  if (bpp > units) bpp = units;
+  if (bpp < 1) bpp = 1;
+  a.blocks_per_pose = (int)bpp;
 }
 
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st) {
+  if (a.variant == 0) return launch_cascade_tiled(a, n_poses, st);
   // grid.x = poses x blocks_per_pose, issued in chunks that fit gridDim.x
   const int64_t max_blocks = (int64_t)1 << 30;
   int64_t chunk = max_blocks / a.blocks_per_pose;
@@ -417,10 +472,13 @@ cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t s
     CascadeArgs c = a;
     c.pose_offset = a.pose_offset + p0;
     unsigned grid = (unsigned)(np * a.blocks_per_pose);
-    if (a.precision == 32)
-      cascade3d_kernel<float><<<grid, kThreads, 0, st>>>(c);
-    else
-      cascade3d_kernel<double><<<grid, kThreads, 0, st>>>(c);
+    if (a.precision == 32) {
+      if (a.wrap) cascade3d_kernel<float, true><<<grid, kThreads, 0, st>>>(c);
+      else cascade3d_kernel<float, false><<<grid, kThreads, 0, st>>>(c);
+    } else {
+      if (a.wrap) cascade3d_kernel<double, true><<<grid, kThreads, 0, st>>>(c);
+      else cascade3d_kernel<double, false><<<grid, kThreads, 0, st>>>(c);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

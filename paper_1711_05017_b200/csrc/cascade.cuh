@@ -29,12 +29,43 @@ struct CascadeArgs {
   int blocks_per_pose;
   int64_t segs_per_block;
   double tie_eps;
+  int variant;           // 0 = u-space tiled (default), 1 = direct gather
+  int tile;              // tiled variant: cells per tile side (8 or 16)
+  int tile_force;        // 0 = auto
+  int smem_bytes;        // tiled variant: dynamic shared memory per CTA
   // cross-block scratch and output
   double* partials;      // n_poses * blocks_per_pose * kNumMoments (if bpp > 1)
   unsigned* counters;    // n_poses, zero-initialised, re-armed by the kernel
   double* out;           // n_poses * 14 (interleaved complex128 x 7)
 };
 
+// 26 moment accumulators (layout = the moment index order used by finalize)
+template <typename T> struct Acc26 {
+  T v[kNumMoments];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < kNumMoments; ++i) v[i] = (T)0;
+  }
+  // S += bV; Z_a += k_a bV; Y[b][a] += k_a X_b
+  template <typename C>
+  __device__ __forceinline__ void add(C bV, C X0, C X1, C X2, T kx, T ky, T kz) {
+    v[0] += bV.re; v[1] += bV.im;
+    v[2] = fma(kx, bV.re, v[2]); v[3] = fma(kx, bV.im, v[3]);
+    v[4] = fma(ky, bV.re, v[4]); v[5] = fma(ky, bV.im, v[5]);
+    v[6] = fma(kz, bV.re, v[6]); v[7] = fma(kz, bV.im, v[7]);
+    const C X[3] = {X0, X1, X2};
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      v[8 + 6 * b] = fma(kx, X[b].re, v[8 + 6 * b]);  v[9 + 6 * b] = fma(kx, X[b].im, v[9 + 6 * b]);
+      v[10 + 6 * b] = fma(ky, X[b].re, v[10 + 6 * b]); v[11 + 6 * b] = fma(ky, X[b].im, v[11 + 6 * b]);
+      v[12 + 6 * b] = fma(kz, X[b].re, v[12 + 6 * b]); v[13 + 6 * b] = fma(kz, X[b].im, v[13 + 6 * b]);
+    }
+  }
+};
+
+int tiled_tile_count(const CascadeArgs& a, int ts);
+size_t tiled_smem_bytes(int precision, int ts, const int w[3]);
+cudaError_t launch_cascade_tiled(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);
 void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks);
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);
 int64_t packed_window_elems(const int w[3]);

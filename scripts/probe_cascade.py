@@ -7,10 +7,20 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(
 from conftest import synthetic_window, random_rotation
 
 rng = np.random.default_rng(0)
+import ctypes
+from paper_1711_05017_b200 import _lib
+_lib.ensure_device(0)
+L = int(os.environ.get('RUNLEN', '0'))
+_lib.check(_lib.LIB.gf_set_cascade_run_length(L))
+VAR = int(os.environ.get('VARIANT', '1'))
+_lib.check(_lib.LIB.gf_set_cascade_variant(VAR))
+_lib.check(_lib.LIB.gf_set_cascade_tile(int(os.environ.get('TILE','0'))))
+WS = [int(x) for x in os.environ.get('WS', '32,64,96,128').split(',')]
+PRECS = os.environ.get('PRECS', 'fp32,fp64').split(',')
 torch.cuda.init()
 print(torch.cuda.get_device_name(), flush=True)
-for prec in ("fp32", "fp64"):
-    for w in (32, 64, 96, 128):
+for prec in PRECS:
+    for w in WS:
         C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
         W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
         dom = (1.0 / (2 * w * 0.05),) * 3
@@ -48,5 +58,5 @@ for prec in ("fp32", "fp64"):
         e1.record(); torch.cuda.synchronize()
         per_pose_us = e0.elapsed_time(e1) * 1e3 / (3 * nb)
         tflops = 240 * w ** 3 / (per_pose_us * 1e-6) / 1e12
-        print(f"{prec} w={w:4d} m'={w**3:8d}  host-query p50={p50:7.1f}us p99={p99:7.1f}us  "
+        print(f"V={VAR} L={L} {prec} w={w:4d} m'={w**3:8d}  host-query p50={p50:7.1f}us p99={p99:7.1f}us  "
               f"serial-dev={ser_us:7.2f}us/q  batch={per_pose_us:8.3f}us/pose ({1e6/per_pose_us:9.0f} poses/s, {tflops:5.1f} TF@240)", flush=True)
