@@ -81,6 +81,8 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double *domega, 
  * FMA-chain kernel on the current device; the roofline denominator of the
  * query/sweep kernels (precision 32 or 64). */
 int gf_measure_fma_peak(int precision, double *tflops);
+/* Launch-overhead probe: host and device microseconds per empty launch. */
+int gf_measure_launch(int n, int blocks, double *host_us, double *dev_us);
 
 /* Tuning knobs for experiments: kernel variant (0 = u-space tiled, the
  * default; 1 = direct gather) and the direct variant's run length along kz

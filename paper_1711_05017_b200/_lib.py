@@ -38,6 +38,7 @@ SIGNATURES = {
     "gf_measure_fma_peak": (ctypes.c_int, [ctypes.c_int, c_dp]),
     "gf_set_cascade_variant": (ctypes.c_int, [ctypes.c_int]),
     "gf_set_cascade_tile": (ctypes.c_int, [ctypes.c_int]),
+    "gf_measure_launch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_dp, c_dp]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),
 }
 

@@ -437,6 +437,12 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
     a.smem_bytes = (int)tiled_smem_bytes(a.precision, a.tile, a.w);
     return;
   }
+  if (n_poses == 1 && a.variant == 1) {
+    a.single = 1;
+    a.blocks_per_pose = single_blocks(a, target_blocks / 2);
+    return;
+  }
+  a.single = 0;
   // direct gather: 16 x 16 mode patches x runs of L along the run axis
   int L = a.seg_len > 0 ? a.seg_len : (n_poses >= target_blocks / 2 ? 8 : 4);
   int wmax = a.w[0] > a.w[1] ? a.w[0] : a.w[1];
@@ -464,6 +470,7 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
 
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st) {
   if (a.variant == 0) return launch_cascade_tiled(a, n_poses, st);
+  if (a.single && n_poses == 1) return launch_cascade_single(a, st);
   // grid.x = poses x blocks_per_pose, issued in chunks that fit gridDim.x
   const int64_t max_blocks = (int64_t)1 << 30;
   int64_t chunk = max_blocks / a.blocks_per_pose;

@@ -33,6 +33,7 @@ struct CascadeArgs {
   int tile;              // tiled variant: cells per tile side (8 or 16)
   int tile_force;        // 0 = auto
   int smem_bytes;        // tiled variant: dynamic shared memory per CTA
+  int single;            // 1: one pose through the latency kernel (cascade_single.cu)
   // cross-block scratch and output
   double* partials;      // n_poses * blocks_per_pose * kNumMoments (if bpp > 1)
   unsigned* counters;    // n_poses, zero-initialised, re-armed by the kernel
@@ -65,6 +66,8 @@ template <typename T> struct Acc26 {
 
 int tiled_tile_count(const CascadeArgs& a, int ts);
 size_t tiled_smem_bytes(int precision, int ts, const int w[3]);
+int single_blocks(const CascadeArgs& a, int sms);
+cudaError_t launch_cascade_single(const CascadeArgs& a, cudaStream_t st);
 cudaError_t launch_cascade_tiled(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);
 void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks);
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);

@@ -7,6 +7,8 @@
 #include "../../include/geofield_b200.h"
 #include "common.cuh"
 
+#include <chrono>
+
 namespace gf {
 namespace {
 
@@ -61,5 +63,42 @@ extern "C" int gf_measure_fma_peak(int precision, double* tflops) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(sink);
+  return 0;
+}
+
+namespace gf {
+namespace {
+__global__ void empty_kernel(int* p) {
+  if (p && threadIdx.x == 0 && blockIdx.x == 0) p[0] = 1;
+}
+}  // namespace
+}  // namespace gf
+
+// Launch-overhead probe: n back-to-back empty launches of `blocks` CTAs on a
+// fresh stream; returns host microseconds per launch and device microseconds
+// per launch (events around the whole sequence).
+extern "C" int gf_measure_launch(int n, int blocks, double* host_us, double* dev_us) {
+  using namespace gf;
+  GF_CHECK(n > 0 && host_us && dev_us, GF_EINVAL, "bad argument");
+  cudaStream_t st;
+  GF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  GF_CUDA(cudaEventCreate(&e0));
+  GF_CUDA(cudaEventCreate(&e1));
+  empty_kernel<<<blocks, 256, 0, st>>>(nullptr);
+  GF_CUDA(cudaStreamSynchronize(st));
+  auto t0 = std::chrono::steady_clock::now();
+  GF_CUDA(cudaEventRecord(e0, st));
+  for (int i = 0; i < n; ++i) empty_kernel<<<blocks, 256, 0, st>>>(nullptr);
+  GF_CUDA(cudaEventRecord(e1, st));
+  auto t1 = std::chrono::steady_clock::now();
+  GF_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  GF_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *host_us = std::chrono::duration<double, std::micro>(t1 - t0).count() / n;
+  *dev_us = 1e3 * ms / n;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
   return 0;
 }
