@@ -77,6 +77,73 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double *domega, 
                       const double *center, int precision, int64_t n, const double *poses_dev, double *out_dev,
                       void *stream);
 
+/* Density construction (stage 1) ------------------------------------------ */
+
+/* Element arrays: 3D triangles (ne x 9 doubles: v0, v1, v2), 2D segments
+ * (ne x 4: a, b); normals (ne x d, outward, unit); measures (ne: triangle
+ * areas / segment lengths).  Points P: m x d doubles.  Host in / host out.
+ * All float64 with every operation separately rounded (bit-exact distances
+ * and decisions against the reference). */
+
+/* Exact min point-element distance and winding number per point; either
+ * output may be NULL.  Replaces _core.distance_{2,3}d (_core.pyx:149-230, via
+ * backend.distance_batch, backend.py:71-93) and _core.winding_{2,3}d
+ * (_core.pyx:262-292, via backend.winding_batch, backend.py:96-113). */
+int gf_distance_winding(int d, const double *elems, int64_t ne, const double *P, int64_t m, double *xi_out,
+                        double *wind_out);
+
+/* Adaptive skeletal sweep I+ per point.  Replaces _core.sweep_{2,3}d
+ * (_core.pyx:300-523) via backend.sweep_batch (backend.py:116-150): out is
+ * interleaved complex128 (m), resid (m) is read and max-updated in place,
+ * clamps (m) are incremented. */
+int gf_sweep(int d, const double *elems, const double *normals, const double *measures, int64_t ne, const double *P,
+             const double *xi_eff, int64_t m, double sigma, double gconst, double max_angle, int max_depth,
+             double eta_min, double *out_c128, double *resid, int64_t *clamps);
+
+/* Whole affinity_field (descriptor.py:309-357) on the grid nodes, device
+ * resident: distance + winding, sweep (family 1 = SkeletalDensity; 0 =
+ * InverseSquare, values = winding), combine, neighbour fill of excluded
+ * nodes.  values_dev: complex128 node values (device); flags_dev: one byte
+ * per node (bit0 excluded, bit1 unresolved, bit2 inside); stats[0] = total
+ * eta clamps, stats[1] = worst residual. */
+int gf_affinity_grid(int d, const double *elems, const double *normals, const double *measures, int64_t ne,
+                     const int32_t *dims, const double *origin, double spacing, int family, double sigma,
+                     double gconst, double lam_in, double lam_out, double max_angle, int max_depth, double eta_floor,
+                     void *values_dev, uint8_t *flags_dev, double *stats, void *stream);
+
+/* Spectra (stage 2) and landscapes (stage 4) ------------------------------ */
+
+/* One batched line-FFT pass along `axis` of a 3D row-major complex array
+ * (2D data: shape (1, n0, n1)); precision 32 (complex64) or 64 (complex128),
+ * device buffers, stream-ordered.  Input element i of a line sits at FFT
+ * position i (in_centered = 0, length n) or (i - Lin/2) mod n (DC-centred
+ * window, zero-padded) and is scaled by exp(2 pi i m in_phase); output
+ * element i reads position i or (i - Lout/2) mod n (centred truncation) and
+ * is scaled by scale * exp(2 pi i m out_phase), m = mode number.  sign -1
+ * forward, +1 inverse (unnormalised).  Three passes realise
+ * spectral.forward_dft / truncate / center_window / inverse_dft
+ * (spectral.py:114-195) and the landscape's zero-padded inverse
+ * (energy.py:336-343). */
+int gf_fft_pass(int precision, const void *in, void *out, const int32_t *shape_in, const int32_t *shape_out,
+                int axis, int n, int in_centered, int out_centered, int sign, double in_phase, double out_phase,
+                double scale, void *stream);
+
+/* Q(w) = C1(w) V(w) exp(2 pi i w.s) over the window, V = multilinear sample
+ * of window h2 at u = -R^T w / dw + w/2 (zero outside unless wrap; float64
+ * floor decisions as the cascade); h1 = 0 means C1 = 1
+ * (rotate_reflect_spectrum, spectral.py:204-226).  out_dev: window-shaped,
+ * complex64/complex128 by precision. */
+int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double *domega, const double *R, const double *s,
+                      int precision, void *out_dev, void *stream);
+
+/* Full translational landscape (energy.score_field, energy.py:309-344):
+ * the product above with s = Rc - c + origin, then three pruned inverse
+ * passes to the dims grid, times scale (= 1 / (N^d dV)).  work_dev holds
+ * >= w N^2 elements, work2_dev >= w^2 N (2D: w, w N), out_dev N^d. */
+int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double *domega, const int32_t *dims, const double *R,
+                   const double *s, double scale, int precision, void *work_dev, void *work2_dev, void *out_dev,
+                   void *stream);
+
 /* Diagnostics: FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured with an
  * FMA-chain kernel on the current device; the roofline denominator of the
  * query/sweep kernels (precision 32 or 64). */

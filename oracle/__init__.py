@@ -103,9 +103,14 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center):
 
 
 def _elements(elems):
+    """Triangles ((n, 3, 3) or flat (n, 9)) -> d = 3; segments ((n, 2, 2) or (n, 4)) -> d = 2."""
     e = _f64(elems)
-    d = e.shape[-1]
-    return e.reshape(len(e), -1), d
+    e = e.reshape(len(e), -1)
+    if e.shape[1] == 9:
+        return e, 3
+    if e.shape[1] == 4:
+        return e, 2
+    raise ValueError("elements must be triangles (n, 9) or segments (n, 4)")
 
 
 def distance(elems, P):

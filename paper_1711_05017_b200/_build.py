@@ -35,14 +35,30 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+# files whose float64 decision path must round every operation separately
+# (bit-exact distances / exclusion / subdivision vs the reference's no-FMA
+# x86-64 build)
+NO_FMA = {"density.cu"}
+
+
 def build(verbose=False, force=False):
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    objdir = os.path.join(HERE, "csrc", "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        flags = [f for f in FLAGS if f != "-shared"]
+        if os.path.basename(src) in NO_FMA:
+            flags.append("-fmad=false")
+        cmd = [NVCC, *flags, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs], check=True)
     return OUT
 
 

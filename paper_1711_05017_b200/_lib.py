@@ -39,6 +39,21 @@ SIGNATURES = {
     "gf_set_cascade_variant": (ctypes.c_int, [ctypes.c_int]),
     "gf_set_cascade_tile": (ctypes.c_int, [ctypes.c_int]),
     "gf_measure_launch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_dp, c_dp]),
+    "gf_distance_winding": (ctypes.c_int, [ctypes.c_int, c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp]),
+    "gf_sweep": (ctypes.c_int, [ctypes.c_int, c_dp, c_dp, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64,
+                                ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                c_dp, c_dp, c_i64p]),
+    "gf_affinity_grid": (ctypes.c_int, [ctypes.c_int, c_dp, c_dp, c_dp, ctypes.c_int64, c_i32p, c_dp,
+                                        ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                        ctypes.c_double, c_vp, c_vp, c_dp, c_vp]),
+    "gf_fft_pass": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_i32p, c_i32p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_double, c_vp]),
+    "gf_rotate_product": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_dp, c_dp,
+                                         ctypes.c_int, c_vp, c_vp]),
+    "gf_score_field": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_i32p, c_dp, c_dp,
+                                      ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),
 }
 

@@ -212,3 +212,77 @@ def cascade_batch(C1, C2, wrap, domega, dcell, center, poses, out=None, precisio
                                _prec_bits(precision), int(n), ctypes.c_void_p(poses.data_ptr()),
                                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# density operators (backend.py:71-150 of the reference)
+
+
+def _elements(solid):
+    return solid.element_arrays()
+
+
+def distance_batch(solid, P, threads=None):
+    """Min distance from each row of P to the solid's boundary elements
+    (exact point-element distance, float64, bit-identical to the reference)."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    _lib.ensure_device()
+    elems, _, _ = _elements(solid)
+    out = np.empty(len(P))
+    if len(P):
+        check(LIB.gf_distance_winding(solid.dimension, dptr(elems), len(elems), dptr(P), len(P), dptr(out), None))
+    return out
+
+
+def winding_batch(solid, P, threads=None):
+    """Exact winding number (sum of per-element subtended angles)."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    _lib.ensure_device()
+    elems, _, _ = _elements(solid)
+    out = np.empty(len(P))
+    if len(P):
+        check(LIB.gf_distance_winding(solid.dimension, dptr(elems), len(elems), dptr(P), len(P), None, dptr(out)))
+    return out
+
+
+def sweep_batch(solid, P, xi_eff, sigma, gconst, max_angle, max_depth, eta_min, threads=None):
+    """Adaptive skeletal quadrature I+ per point; (values, residuals, clamp count)."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    xi_eff = np.ascontiguousarray(xi_eff, dtype=np.float64)
+    _lib.ensure_device()
+    elems, normals, measures = _elements(solid)
+    out = np.empty(len(P), dtype=np.complex128)
+    resid = np.zeros(len(P))
+    clamps = np.zeros(len(P), dtype=np.int64)
+    if len(P):
+        check(LIB.gf_sweep(solid.dimension, dptr(elems), dptr(np.ascontiguousarray(normals)), dptr(measures),
+                           len(elems), dptr(P), dptr(xi_eff), len(P), float(sigma), float(gconst),
+                           float(max_angle), int(max_depth), float(eta_min), dptr(out.view(np.float64)),
+                           dptr(resid), clamps.ctypes.data_as(_lib.c_i64p)))
+    return out, resid, int(clamps.sum())
+
+
+def affinity_grid(solid, grid, family, sigma, gconst, lam_in, lam_out, max_angle, max_depth, eta_floor):
+    """The whole affinity pipeline on the grid nodes, device resident.
+
+    Returns (values: CUDA complex128 tensor of grid.node_count, flags: CUDA
+    uint8 tensor (bit0 excluded, bit1 unresolved, bit2 inside), stats
+    (total clamps, worst residual))."""
+    import torch
+
+    dev = _lib.ensure_device()
+    elems, normals, measures = _elements(solid)
+    m = grid.node_count
+    values = torch.empty(m, dtype=torch.complex128, device=f"cuda:{dev}")
+    flags = torch.empty(m, dtype=torch.uint8, device=f"cuda:{dev}")
+    stats = np.zeros(2)
+    dims = (ctypes.c_int32 * 3)(*(list(grid.dims) + [1] * (3 - len(grid.dims))))
+    origin = np.zeros(3)
+    origin[:grid.dimension] = grid.origin
+    st = torch.cuda.current_stream(values.device).cuda_stream
+    check(LIB.gf_affinity_grid(grid.dimension, dptr(elems), dptr(np.ascontiguousarray(normals)), dptr(measures),
+                               len(elems), dims, dptr(origin), float(grid.spacing), int(family), float(sigma),
+                               float(gconst), float(lam_in), float(lam_out), float(max_angle), int(max_depth),
+                               float(eta_floor), ctypes.c_void_p(values.data_ptr()),
+                               ctypes.c_void_p(flags.data_ptr()), dptr(stats), ctypes.c_void_p(st)))
+    return values, flags, (int(stats[0]), float(stats[1]))

@@ -186,6 +186,31 @@ static void embed_pose(int d, const double* R, const double* t, double* dst) {
   }
 }
 
+// Operand views for the field kernels: raw C1 (h1 == 0 -> null, meaning
+// C1 = 1) and the padded, z-pair-packed C2 at the requested precision.
+int window_operands(uint64_t h1, uint64_t h2, int wrap, int precision, cudaStream_t st, const void** c1_raw,
+                    const void** c2_packed, int w[3], int* dim) {
+  GF_CHECK(precision == 32 || precision == 64, GF_EINVAL, "precision must be 32 or 64");
+  int rc = ensure_context();
+  if (rc) return rc;
+  Window* w2 = find_window(h2);
+  GF_CHECK(w2, GF_EINVAL, "unknown window handle");
+  *c1_raw = nullptr;
+  if (h1) {
+    Window* w1 = find_window(h1);
+    GF_CHECK(w1, GF_EINVAL, "unknown window handle");
+    GF_CHECK(w1->d == w2->d, GF_EINVAL, "window dimension mismatch");
+    for (int ax = 0; ax < 3; ++ax) GF_CHECK(w1->w[ax] == w2->w[ax], GF_EINVAL, "window shape mismatch");
+    rc = window_raw(w1, precision, st, c1_raw);
+    if (rc) return rc;
+  }
+  rc = window_packed(w2, precision, wrap, st, c2_packed);
+  if (rc) return rc;
+  for (int ax = 0; ax < 3; ++ax) w[ax] = w2->w[ax];
+  *dim = w2->d;
+  return 0;
+}
+
 }  // namespace gf
 
 using namespace gf;

@@ -25,7 +25,6 @@ namespace gf {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 
 struct SinglePose {
   double mu[3][3];

@@ -1,0 +1,207 @@
+// field.cu -- full translational landscape (stage 4, F1/F2) and the rotated
+// spectrum resampler.
+//
+// Reference: energy.score_field (/root/reference/pkg/src/geofield/
+// energy.py:309-344) forms Q(w) = C1(w) V(w) exp(2 pi i w.(Rc - c)), with V
+// the multilinear sample of C2 at u = -R^T w / dw + w/2
+// (_fallback._interp_window, _fallback.py:312-351), embeds Q in the full
+// DC-centred grid, multiplies by the origin phases and inverse-FFTs, / dV.
+//
+// Here the product kernel evaluates Q straight into the window (one thread
+// per retained mode; same continuous index and float64 floor tie-break as
+// the cascade kernels), with the origin phase folded into the same
+// separable phase, and three pruned inverse passes (fft.cu) expand the w^d
+// window to the N^d landscape with scale dcell = 1 / (N^d dV).  The same
+// product kernel with C1 = 1 gives rotate_reflect_spectrum
+// (spectral.py:204-226).
+#include "../../include/geofield_b200.h"
+#include "cascade.cuh"
+#include "common.cuh"
+
+#include <math.h>
+
+extern "C" int gf_fft_pass(int precision, const void* in, void* out, const int32_t* shape_in,
+                           const int32_t* shape_out, int axis, int n, int in_centered, int out_centered, int sign,
+                           double in_phase, double out_phase, double scale, void* stream);
+
+namespace gf {
+
+// window handle internals (capi.cu)
+int window_operands(uint64_t h1, uint64_t h2, int wrap, int precision, cudaStream_t st, const void** c1_raw,
+                    const void** c2_packed, int w[3], int* dim);
+
+namespace {
+
+struct RotArgs {
+  const void* C1;  // raw window (null: C1 = 1)
+  const void* C2p; // packed moving window
+  int w[3];
+  int dim;
+  double dom[3];
+  double R[9];
+  double s[3];     // phase exp(2 pi i w.s)
+  double tie_eps;
+  void* out;       // window-shaped complex<T>
+};
+
+__device__ __forceinline__ double exact_u_f(const double* R, const double* dom, int a, int kx, int ky, int kz, int hx,
+                                            int hy, int hz, int ha) {
+  double ox = __dmul_rn((double)(kx - hx), dom[0]);
+  double oy = __dmul_rn((double)(ky - hy), dom[1]);
+  double oz = __dmul_rn((double)(kz - hz), dom[2]);
+  double s = __dadd_rn(__dadd_rn(__dmul_rn(R[0 + a], ox), __dmul_rn(R[3 + a], oy)), __dmul_rn(R[6 + a], oz));
+  return __dadd_rn(__ddiv_rn(-s, dom[a]), (double)ha);
+}
+
+template <typename T, bool WRAP>
+__global__ void __launch_bounds__(256) rotate_product_kernel(RotArgs a) {
+  using P4 = typename pair4<T>::type;
+  const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
+  const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
+  const int64_t n = (int64_t)w0 * w1 * w2;
+  const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
+  const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
+  const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
+  cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
+  // mu[a][b] = -R[b][a] dw_b / dw_a
+  double mu[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) mu[i][j] = -a.R[j * 3 + i] * (a.dom[j] / a.dom[i]);
+  const T eps = (T)a.tie_eps;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int kz = (int)(e % w2);
+    const int64_t r = e / w2;
+    const int ky = (int)(r % w1), kx = (int)(r / w1);
+    const double kap[3] = {(double)(kx - hx), (double)(ky - hy), (double)(kz - hz)};
+    T fl[3], f[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      double h = ax == 0 ? hx : (ax == 1 ? hy : hz);
+      T u = (T)(h + mu[ax][0] * kap[0] + mu[ax][1] * kap[1] + mu[ax][2] * kap[2]);
+      fl[ax] = floor(u);
+      f[ax] = u - fl[ax];
+      const bool tie = (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
+      if (tie) {
+        double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+        double fe = floor(ue);
+        fl[ax] = (T)fe;
+        f[ax] = (T)(ue - fe);
+      }
+    }
+    int ix = (int)fl[0], iy = (int)fl[1], iz = (int)fl[2];
+    cx<T> V = mk<T>(0, 0);
+    bool live = true;
+    if (WRAP) {
+      ix = ((ix % w0) + w0) % w0;
+      iy = ((iy % w1) + w1) % w1;
+      iz = ((iz % w2) + w2) % w2;
+    } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
+               (unsigned)(iz + 1) > (unsigned)w2) {
+      live = false;
+    }
+    if (live) {
+      const P4* p = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
+      P4 e00 = ldg_pair(p), e10 = ldg_pair(p + sx), e01 = ldg_pair(p + sy), e11 = ldg_pair(p + sx + sy);
+      const T fu = f[0], fv = f[1], fs = f[2];
+      cx<T> a00 = lerp(mk<T>(e00.x, e00.y), mk<T>(e10.x, e10.y), fu);
+      cx<T> a01 = lerp(mk<T>(e00.z, e00.w), mk<T>(e10.z, e10.w), fu);
+      cx<T> a10 = lerp(mk<T>(e01.x, e01.y), mk<T>(e11.x, e11.y), fu);
+      cx<T> a11 = lerp(mk<T>(e01.z, e01.w), mk<T>(e11.z, e11.w), fu);
+      V = lerp(lerp(a00, a10, fv), lerp(a01, a11, fv), fs);
+    }
+    // separable phase exp(2 pi i sum_a kappa_a dw_a s_a), reduced in float64
+    double cyc = 0.0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      double c = a.dom[ax] * a.s[ax] * kap[ax];
+      cyc += c - rint(c);
+    }
+    cyc -= rint(cyc);
+    double sn, cs;
+    sincospi(2.0 * cyc, &sn, &cs);
+    cx<T> q = V * mk<T>((T)cs, (T)sn);
+    if (C1) q = C1[e] * q;
+    out[e] = q;
+  }
+}
+
+}  // namespace
+}  // namespace gf
+
+using namespace gf;
+
+extern "C" {
+
+int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double* domega, const double* R, const double* s,
+                      int precision, void* out_dev, void* stream) {
+  GF_CHECK(domega && R && s && out_dev, GF_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  RotArgs a = {};
+  int rc = window_operands(h1, h2, wrap, precision, st, &a.C1, &a.C2p, a.w, &a.dim);
+  if (rc) return rc;
+  for (int k = 0; k < 3; ++k) {
+    a.dom[k] = k < a.dim ? domega[k] : 1.0;
+    a.s[k] = k < a.dim ? s[k] : 0.0;
+  }
+  if (a.dim == 3) {
+    for (int k = 0; k < 9; ++k) a.R[k] = R[k];
+  } else {
+    const double e[9] = {R[0], R[1], 0.0, R[2], R[3], 0.0, 0.0, 0.0, 1.0};
+    for (int k = 0; k < 9; ++k) a.R[k] = e[k];
+  }
+  double umax = 0.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    double v = a.w[ax] / 2;
+    for (int b = 0; b < 3; ++b) v += (a.dom[b] / a.dom[ax]) * (a.w[b] / 2 + 1);
+    umax = v > umax ? v : umax;
+  }
+  double eps = 8.0 * ldexp(umax, precision == 32 ? -23 : -52);
+  double floor_eps = precision == 32 ? 1e-4 : 1e-9;
+  a.tie_eps = eps > floor_eps ? eps : floor_eps;
+  a.out = out_dev;
+  int64_t n = (int64_t)a.w[0] * a.w[1] * a.w[2];
+  unsigned grid = (unsigned)(ceil_div(n, 256) < 148 * 16 ? ceil_div(n, 256) : 148 * 16);
+  if (precision == 32) {
+    if (wrap) rotate_product_kernel<float, true><<<grid, 256, 0, st>>>(a);
+    else rotate_product_kernel<float, false><<<grid, 256, 0, st>>>(a);
+  } else {
+    if (wrap) rotate_product_kernel<double, true><<<grid, 256, 0, st>>>(a);
+    else rotate_product_kernel<double, false><<<grid, 256, 0, st>>>(a);
+  }
+  GF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double* domega, const int32_t* dims, const double* R,
+                   const double* s, double scale, int precision, void* work_dev, void* work2_dev, void* out_dev,
+                   void* stream) {
+  GF_CHECK(dims && work_dev && work2_dev && out_dev, GF_EINVAL, "null argument");
+  int rc = gf_rotate_product(h1, h2, wrap, domega, R, s, precision, work_dev, stream);
+  if (rc) return rc;
+  const void* c1;
+  const void* c2;
+  int w[3], dim;
+  rc = window_operands(h1, h2, wrap, precision, (cudaStream_t)stream, &c1, &c2, w, &dim);
+  if (rc) return rc;
+  // three pruned inverse passes: window-centred in, node order out
+  int32_t N[3] = {dim == 3 ? dims[0] : 1, dim == 3 ? dims[1] : dims[0], dim == 3 ? dims[2] : dims[1]};
+  int32_t W[3] = {dim == 3 ? w[0] : 1, dim == 3 ? w[1] : w[0], dim == 3 ? w[2] : w[1]};
+  int32_t sh0[3] = {W[0], W[1], W[2]};
+  int32_t sh1[3] = {W[0], W[1], N[2]};
+  int32_t sh2[3] = {W[0], N[1], N[2]};
+  int32_t sh3[3] = {N[0], N[1], N[2]};
+  rc = gf_fft_pass(precision, work_dev, work2_dev, sh0, sh1, 2, N[2], 1, 0, 1, 0.0, 0.0, 1.0, stream);
+  if (rc) return rc;
+  if (dim == 3) {
+    rc = gf_fft_pass(precision, work2_dev, work_dev, sh1, sh2, 1, N[1], 1, 0, 1, 0.0, 0.0, 1.0, stream);
+    if (rc) return rc;
+    rc = gf_fft_pass(precision, work_dev, out_dev, sh2, sh3, 0, N[0], 1, 0, 1, 0.0, 0.0, scale, stream);
+  } else {
+    rc = gf_fft_pass(precision, work2_dev, out_dev, sh1, sh2, 1, N[1], 1, 0, 1, 0.0, 0.0, scale, stream);
+  }
+  return rc;
+}
+
+}  // extern "C"
