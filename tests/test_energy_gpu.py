@@ -42,7 +42,7 @@ def test_evaluate_matches_reference_golden(peg_assets, prec, rtol):
             assert res.modes_used == (mp or 4096)
             np.testing.assert_allclose(got, want, rtol=rtol, atol=rtol * np.max(np.abs(want)))
     finally:
-        backend.set_precision(prec if False else prev)
+        backend.set_precision(prev)
 
 
 def test_score_matches_brute_at_lattice_rotations():
