@@ -136,6 +136,12 @@ int gf_fft_pass(int precision, const void *in, void *out, const int32_t *shape_i
 int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double *domega, const double *R, const double *s,
                       int precision, void *out_dev, void *stream);
 
+/* Same restricted to window x-planes [kx0, kx0 + nkx) (nkx < 0: all); out
+ * is (nkx, w1, w2).  The slab-decomposed landscape gives each rank its own
+ * kx-planes. */
+int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double *domega, const double *R,
+                             const double *s, int precision, int kx0, int nkx, void *out_dev, void *stream);
+
 /* Full translational landscape (energy.score_field, energy.py:309-344):
  * the product above with s = Rc - c + origin, then three pruned inverse
  * passes to the dims grid, times scale (= 1 / (N^d dV)).  work_dev holds

@@ -41,7 +41,8 @@ struct RotArgs {
   double R[9];
   double s[3];     // phase exp(2 pi i w.s)
   double tie_eps;
-  void* out;       // window-shaped complex<T>
+  int kx0, nkx;    // window x-planes [kx0, kx0 + nkx) (slab decomposition)
+  void* out;       // (nkx, w1, w2) complex<T>
 };
 
 __device__ __forceinline__ double exact_u_f(const double* R, const double* dom, int a, int kx, int ky, int kz, int hx,
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(256) rotate_product_kernel(RotArgs a) {
   using P4 = typename pair4<T>::type;
   const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
-  const int64_t n = (int64_t)w0 * w1 * w2;
+  const int64_t n = (int64_t)a.nkx * w1 * w2;
   const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
   const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
   const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(256) rotate_product_kernel(RotArgs a) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int kz = (int)(e % w2);
     const int64_t r = e / w2;
-    const int ky = (int)(r % w1), kx = (int)(r / w1);
+    const int ky = (int)(r % w1), kx = a.kx0 + (int)(r / w1);
     const double kap[3] = {(double)(kx - hx), (double)(ky - hy), (double)(kz - hz)};
     T fl[3], f[3];
 #pragma unroll
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) rotate_product_kernel(RotArgs a) {
     double sn, cs;
     sincospi(2.0 * cyc, &sn, &cs);
     cx<T> q = V * mk<T>((T)cs, (T)sn);
-    if (C1) q = C1[e] * q;
+    if (C1) q = C1[((int64_t)kx * w1 + ky) * w2 + kz] * q;
     out[e] = q;
   }
 }
@@ -134,13 +135,21 @@ using namespace gf;
 
 extern "C" {
 
-int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double* domega, const double* R, const double* s,
-                      int precision, void* out_dev, void* stream) {
+int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double* domega, const double* R,
+                             const double* s, int precision, int kx0, int nkx, void* out_dev, void* stream) {
   GF_CHECK(domega && R && s && out_dev, GF_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
   RotArgs a = {};
   int rc = window_operands(h1, h2, wrap, precision, st, &a.C1, &a.C2p, a.w, &a.dim);
   if (rc) return rc;
+  if (nkx < 0) {
+    kx0 = 0;
+    nkx = a.w[0];
+  }
+  GF_CHECK(kx0 >= 0 && kx0 + nkx <= a.w[0], GF_EINVAL, "plane range outside the window");
+  a.kx0 = kx0;
+  a.nkx = nkx;
+  if (nkx == 0) return 0;
   for (int k = 0; k < 3; ++k) {
     a.dom[k] = k < a.dim ? domega[k] : 1.0;
     a.s[k] = k < a.dim ? s[k] : 0.0;
@@ -161,7 +170,7 @@ int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   double floor_eps = precision == 32 ? 1e-4 : 1e-9;
   a.tie_eps = eps > floor_eps ? eps : floor_eps;
   a.out = out_dev;
-  int64_t n = (int64_t)a.w[0] * a.w[1] * a.w[2];
+  int64_t n = (int64_t)a.nkx * a.w[1] * a.w[2];
   unsigned grid = (unsigned)(ceil_div(n, 256) < 148 * 16 ? ceil_div(n, 256) : 148 * 16);
   if (precision == 32) {
     if (wrap) rotate_product_kernel<float, true><<<grid, 256, 0, st>>>(a);
@@ -172,6 +181,11 @@ int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   }
   GF_CUDA(cudaGetLastError());
   return 0;
+}
+
+int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double* domega, const double* R, const double* s,
+                      int precision, void* out_dev, void* stream) {
+  return gf_rotate_product_planes(h1, h2, wrap, domega, R, s, precision, 0, -1, out_dev, stream);
 }
 
 int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double* domega, const int32_t* dims, const double* R,

@@ -1,0 +1,205 @@
+"""Multi-GPU paths: one process per GPU.
+
+* Pose sweep (Q3): poses are independent units -> contiguous pose ranges per
+  rank, no collective in the loop; results are optionally all-gathered once.
+  The reference has no sweep (it loops evaluate() serially, cli.py:349-356).
+* Landscape (F1) at large N: slab decomposition with one exchange step.
+  Rank r owns window x-planes [a_r, b_r): it forms its Q planes (product
+  kernel restricted to those planes) and runs the two inner inverse passes
+  (z then y: w -> N), giving (b_r - a_r, N1, N2).  An all-to-all re-slices
+  the data by output y-slabs (each rank gets every x-plane of its y-range),
+  and the last pass inverts along x (w0 -> N0).  Rank r ends with the
+  landscape rows y in [c_r, d_r): an (N0, d_r - c_r, N2) slab.
+* The single haptic query does not shard: replicas only.
+
+The decomposition logic (ranges, split sizes, re-assembly) is host code that
+runs the same with NCCL on GPUs and gloo on CPUs; `tests/test_parallel.py`
+drives it with gloo at world size 2.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib, backend
+
+
+def shard_range(n, rank, world):
+    """Contiguous [lo, hi) share of n units for `rank` (balanced to +-1)."""
+    base, extra = divmod(int(n), int(world))
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def _world(group):
+    dist = _dist()
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+# ---------------------------------------------------------------------------
+# pose sweep
+
+
+def gather_rows(local, n_total, group=None):
+    """All-gather per-rank row blocks (contiguous shard_range layout) into
+    the full (n_total, ...) array on every rank; works for NCCL and gloo."""
+    import torch
+
+    rank, world = _world(group)
+    if world == 1:
+        return local
+    dist = _dist()
+    rows = [shard_range(n_total, r, world) for r in range(world)]
+    width = max(hi - lo for lo, hi in rows)
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[: hi - lo] for b, (lo, hi) in zip(bufs, rows)], dim=0)
+
+
+def pose_sweep(asset1, asset2, rotations, translations, m_prime=None, precision=None, group=None, gather=True,
+               compute=None):
+    """Evaluate many poses, sharded by pose across the ranks of `group`.
+
+    rotations (n, d, d), translations (n, d) (host arrays, the same on every
+    rank).  Returns a (n, 7) complex128 host array [S, T..., G...] (2D: 4
+    columns) when gather, else this rank's (hi - lo, 7) shard and its range.
+    `compute(asset1, asset2, R_shard, t_shard)` may replace the GPU kernel
+    (tests run the decomposition on CPU with the oracle)."""
+    import torch
+
+    rank, world = _world(group)
+    R = np.asarray(rotations, dtype=np.float64)
+    t = np.asarray(translations, dtype=np.float64)
+    n = len(t)
+    lo, hi = shard_range(n, rank, world)
+    if compute is None:
+        local = _sweep_gpu(asset1, asset2, R[lo:hi], t[lo:hi], m_prime, precision)
+    else:
+        local = torch.as_tensor(compute(asset1, asset2, R[lo:hi], t[lo:hi]))
+    if not gather:
+        return local.cpu().numpy(), (lo, hi)
+    full = gather_rows(torch.view_as_real(local.contiguous()) if local.is_complex() else local, n, group)
+    if not full.is_complex():
+        full = torch.view_as_complex(full.contiguous())
+    return full.cpu().numpy()
+
+
+def _sweep_gpu(asset1, asset2, R, t, m_prime, precision):
+    """Local shard through the batched cascade kernel; (k, 7) complex128 CUDA tensor."""
+    import torch
+
+    g = asset1.grid
+    c = g.center()
+    C1, wrap1 = asset1.window(m_prime)
+    C2, wrap2 = asset2.window(m_prime)
+    t_eff = t - c + np.einsum("nij,j->ni", R, c) if len(t) else t
+    poses = torch.from_numpy(backend.pack_poses(R, t_eff)).to(f"cuda:{_lib.ensure_device()}")
+    dcell = 1.0 / (g.node_count * g.cell_volume)
+    out = backend.cascade_batch(C1, C2, wrap1 and wrap2, g.delta_omega(), dcell, c, poses, precision=precision)
+    res = torch.view_as_complex(out.reshape(-1, 7, 2))
+    if g.dimension == 2:
+        res = res[:, [0, 1, 2, 6]]
+    return res
+
+
+# ---------------------------------------------------------------------------
+# slab-decomposed landscape
+
+
+def slab_plan(window, dims, world):
+    """Per-rank window x-plane ranges and output y-slab ranges."""
+    kx = [shard_range(window[0], r, world) for r in range(world)]
+    ys = [shard_range(dims[1], r, world) for r in range(world)]
+    return kx, ys
+
+
+def exchange_planes_to_slabs(local, kx_ranges, y_ranges, rank, group=None):
+    """All-to-all: local (nk_r, N1, N2) x-planes -> (w0, ny_r, N2) y-slab.
+
+    Works on real tensors (complex data travels as view_as_real)."""
+    import torch
+
+    dist = _dist()
+    world = len(kx_ranges)
+    nk = local.shape[0]
+    tail = tuple(local.shape[2:])
+    send = torch.cat([local[:, lo:hi].reshape(-1) for lo, hi in y_ranges])
+    in_splits = [nk * (hi - lo) * int(np.prod(tail)) for lo, hi in y_ranges]
+    ny = y_ranges[rank][1] - y_ranges[rank][0]
+    out_splits = [(khi - klo) * ny * int(np.prod(tail)) for klo, khi in kx_ranges]
+    recv = torch.empty(sum(out_splits), dtype=local.dtype, device=local.device)
+    if world == 1:
+        recv.copy_(send)
+    else:
+        dist.all_to_all_single(recv, send, out_splits, in_splits, group=group)
+    parts = torch.split(recv, out_splits)
+    blocks = [p.reshape((khi - klo, ny) + tail) for p, (klo, khi) in zip(parts, kx_ranges)]
+    return torch.cat(blocks, dim=0)
+
+
+def score_field_slab(asset1, asset2, R, m_prime=None, precision=64, group=None):
+    """This rank's y-slab (N0, ny, N2) of the landscape (energy.score_field),
+    as a CUDA complex tensor; one all-to-all between the inner passes and the
+    x pass.  Gather the slabs along axis 1 for the full N^3 field."""
+    import torch
+
+    from .energy import _check_pair
+    from .spectral import check_rotation
+
+    _check_pair(asset1, asset2)
+    g = asset1.grid
+    if g.dimension != 3:
+        raise ValueError("slab decomposition is for 3D landscapes")
+    R = check_rotation(R, 3)
+    rank, world = _world(group)
+    C1, wrap1 = asset1.window(m_prime)
+    C2, wrap2 = asset2.window(m_prime)
+    wrap = wrap1 and wrap2
+    w = list(C1.shape)
+    N = list(g.dims)
+    kx_r, y_r = slab_plan(w, N, world)
+    klo, khi = kx_r[rank]
+    nk = khi - klo
+    dtype = torch.complex128 if precision == 64 else torch.complex64
+    dev = f"cuda:{_lib.ensure_device()}"
+    st = torch.cuda.current_stream().cuda_stream
+    c = g.center()
+    s = np.ascontiguousarray(R @ c - c + np.asarray(g.origin), dtype=np.float64)
+    dom = np.ascontiguousarray(g.delta_omega(), dtype=np.float64)
+    q = torch.empty((nk, w[1], w[2]), dtype=dtype, device=dev)
+    _lib.check(_lib.LIB.gf_rotate_product_planes(C1.handle, C2.handle, int(bool(wrap)), _lib.dptr(dom),
+                                                 _lib.dptr(np.ascontiguousarray(R)), _lib.dptr(s), precision, klo, nk,
+                                                 ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(st)))
+    a = _pass(q, (nk, w[1], N[2]), 2, N[2], 1.0, precision)
+    b = _pass(a, (nk, N[1], N[2]), 1, N[1], 1.0, precision)
+    slab = exchange_planes_to_slabs(torch.view_as_real(b), kx_r, y_r, rank, group)
+    slab = torch.view_as_complex(slab.contiguous())
+    ny = y_r[rank][1] - y_r[rank][0]
+    scale = 1.0 / (g.node_count * g.cell_volume)
+    return _pass(slab, (N[0], ny, N[2]), 0, N[0], scale, precision)
+
+
+def _pass(x, out_shape, axis, n, scale, precision):
+    import torch
+
+    out = torch.empty(out_shape, dtype=x.dtype, device=x.device)
+    if x.numel() == 0 or out.numel() == 0:
+        return out
+    si = (ctypes.c_int32 * 3)(*x.shape)
+    so = (ctypes.c_int32 * 3)(*out_shape)
+    st = torch.cuda.current_stream(x.device).cuda_stream
+    _lib.check(_lib.LIB.gf_fft_pass(precision, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), si, so,
+                                    axis, n, 1, 0, 1, 0.0, 0.0, float(scale), ctypes.c_void_p(st)))
+    return out
