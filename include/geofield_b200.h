@@ -142,6 +142,12 @@ int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double *domega, 
 int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double *domega, const double *R,
                              const double *s, int precision, int kx0, int nkx, void *out_dev, void *stream);
 
+/* Fused landscape pass 1 for 3D windows: the product (as above, s given)
+ * for window x-planes [kx0, kx0 + nkx) (nkx < 0: all), inverse-transformed
+ * along z in registers: out (nkx, w1, n2), n2 in {32, ..., 512}. */
+int gf_field_zpass(uint64_t h1, uint64_t h2, int wrap, const double *domega, int n2, const double *R, const double *s,
+                   int precision, int kx0, int nkx, void *out_dev, void *stream);
+
 /* Full translational landscape (energy.score_field, energy.py:309-344):
  * the product above with s = Rc - c + origin, then three pruned inverse
  * passes to the dims grid, times scale (= 1 / (N^d dV)).  work_dev holds

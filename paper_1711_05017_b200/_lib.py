@@ -54,6 +54,8 @@ SIGNATURES = {
                                          ctypes.c_int, c_vp, c_vp]),
     "gf_rotate_product_planes": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_dp, c_dp,
                                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
+    "gf_field_zpass": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_int, c_dp, c_dp,
+                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
     "gf_score_field": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_i32p, c_dp, c_dp,
                                       ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),

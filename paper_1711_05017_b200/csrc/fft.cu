@@ -2,34 +2,36 @@
 //
 // The reference computes its spectra with numpy's pocketfft
 // (spectral.forward_dft / inverse_dft, spectral.py:114-130; the landscape's
-// inverse, energy.py:343).  Here each pass transforms every line of one axis
-// in shared memory with a radix-2 Stockham FFT (natural order in and out),
-// and folds in the index bookkeeping the reference does with
-// fftshift / ifftshift / truncation and per-axis phase ramps:
+// inverse, energy.py:343).  Each pass here transforms every line of one axis
+// with a mixed-radix Stockham FFT (radix-8 stages, one radix-4/2 stage when
+// needed) whose butterflies run in registers: a thread owns 8 points of a
+// line per stage, exchanges go through one shared-memory line buffer, the
+// first stage reads global memory and the last writes it directly, so each
+// pass costs one HBM read and one HBM write of what it touches.
 //
+// Index bookkeeping of the reference (fftshift / ifftshift / truncation /
+// per-axis phase ramps) is folded into the loads and stores:
 //   input  element i of a line sits at FFT position
 //            i                      (node order, in_centered = 0)
 //            (i - Lin/2) mod N      (DC-centred window of Lin modes, zero-padded)
-//          and is multiplied by exp(2 pi i m in_phase), m its mode number;
+//          times exp(2 pi i m in_phase), m its mode number;
 //   output element i reads FFT position
 //            i                      (node order)
 //            (i - Lout/2) mod N     (DC-centred window of Lout modes: truncation)
-//          times exp(2 pi i m out_phase) * scale.
+//          times scale * exp(2 pi i m out_phase).
+// Phases 0 and 1/2 ((-1)^m, the centred-DFT identity) cost nothing.
 //
-// So a forward centred window C = dV fftshift(fftn(ifftshift f))[window] is
-// three passes with out_phase = 1/2 ((-1)^m) and only Lout = w outputs per
-// line written: every later pass reads w/N of the previous volume.  The
-// landscape's zero-padded inverse reads only the w^d window (in_centered).
-//
-// Tile: one CTA owns B lines of length N.  For the contiguous axis the B
-// lines are consecutive in memory; for the other axes the B lines are B
-// consecutive positions of the last axis -- in both cases global loads and
-// stores are coalesced.  Twiddles come from a per-CTA shared table built
-// with sincospi (float64).
+// Tile: one CTA owns B lines; threads (b fastest) so that for strided axes
+// the B lines are B consecutive positions of the contiguous axis -- global
+// accesses are coalesced for every axis.
 #include "../../include/geofield_b200.h"
 #include "common.cuh"
+#include "fft_core.cuh"
 
 #include <math.h>
+
+#include <map>
+#include <mutex>
 
 namespace gf {
 namespace {
@@ -37,158 +39,203 @@ namespace {
 struct FftArgs {
   const void* in;
   void* out;
+  const void* tw;  // twiddle table W_N^m = exp(sign 2 pi i m / N), m < N
   int shape_in[3];
   int shape_out[3];
   int axis;
-  int N;
   int in_centered, out_centered;
-  int sign;  // -1 forward, +1 inverse
+  int sign;
+  int in_phase_kind, out_phase_kind;  // 0: none, 1: (-1)^m, 2: general
   double in_phase, out_phase, scale;
-  int B;     // lines per CTA
 };
 
-template <typename T>
-__global__ void __launch_bounds__(256) fft_lines_kernel(FftArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int N = a.N, B = a.B, half = N >> 1;
-  const int ld = N + 1;  // padded line stride (complex elements)
-  cx<T>* buf0 = reinterpret_cast<cx<T>*>(smem_raw);
-  cx<T>* buf1 = buf0 + B * ld;
-  cx<T>* tw = buf1 + B * ld;  // N/2 twiddles
+// One CTA: B lines x (N / 8) threads (N >= 8), b fastest.
+template <typename T, int N, int B>
+__global__ void __launch_bounds__(B*(N >= 8 ? N / 8 : 1)) fft_kernel(FftArgs a) {
+  constexpr int TPL = FftShape<N>::TPL;  // threads per line
+  constexpr int PT = FftShape<N>::PT;    // points per thread
+  constexpr int LD = LineLD<T, N>::value;  // padded line stride
+  extern __shared__ __align__(16) unsigned char fft_smem[];
+  cx<T>* buf = reinterpret_cast<cx<T>*>(fft_smem);
+  const int tid = threadIdx.x;
   const int ax = a.axis;
+  // contiguous axis: lanes walk along a line (coalesced 8-16 B x 32);
+  // strided axes: lanes walk across B adjacent lines (B x element >= 128 B)
+  const int b = ax == 2 ? tid / TPL : tid % B;
+  const int j = ax == 2 ? tid % TPL : tid / B;  // thread index within the line
   const int Lin = a.shape_in[ax], Lout = a.shape_out[ax];
-  const int tid = threadIdx.x, nt = blockDim.x;
-
-  for (int k = tid; k < half; k += nt) {
-    double s, c;
-    sincospi((double)a.sign * 2.0 * (double)k / (double)N, &s, &c);
-    tw[k] = mk<T>((T)c, (T)s);
-  }
-
-  // line tile decode: shapes (s0, s1, s2); contiguous axis 2
-  const int s2i = a.shape_in[2];
-  int64_t base_in, base_out, stride_in, stride_out, lstep_in, lstep_out;
-  int nlines;  // lines in this tile
-  if (ax == 2) {
-    const int64_t lines = (int64_t)a.shape_in[0] * a.shape_in[1];
-    const int64_t l0 = (int64_t)blockIdx.x * B;
-    nlines = (int)min((int64_t)B, lines - l0);
-    base_in = l0 * Lin;
-    base_out = l0 * Lout;
-    stride_in = 1;
-    stride_out = 1;
-    lstep_in = Lin;
-    lstep_out = Lout;
-  } else {
-    // lines = other-axis index o (size so) x last-axis position p (size s2)
-    const int so = ax == 0 ? a.shape_in[1] : a.shape_in[0];
-    const int ptiles = (s2i + B - 1) / B;
-    const int o = blockIdx.x / ptiles, p0 = (blockIdx.x % ptiles) * B;
-    nlines = min(B, s2i - p0);
-    (void)so;
-    if (ax == 0) {  // element (j, o, p): ((j * s1 + o) * s2 + p)
-      base_in = (int64_t)o * s2i + p0;
-      base_out = (int64_t)o * a.shape_out[2] + p0;
-      stride_in = (int64_t)a.shape_in[1] * s2i;
-      stride_out = (int64_t)a.shape_out[1] * a.shape_out[2];
-    } else {        // ax == 1, element (o, j, p)
-      base_in = (int64_t)o * a.shape_in[1] * s2i + p0;
-      base_out = (int64_t)o * a.shape_out[1] * a.shape_out[2] + p0;
-      stride_in = s2i;
-      stride_out = a.shape_out[2];
-    }
-    lstep_in = 1;
-    lstep_out = 1;
-  }
   const cx<T>* __restrict__ in = reinterpret_cast<const cx<T>*>(a.in);
   cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
+  const cx<T>* __restrict__ tw = reinterpret_cast<const cx<T>*>(a.tw);
 
-  // zero-fill then scatter the inputs to their FFT positions
-  for (int e = tid; e < B * ld; e += nt) buf0[e] = mk<T>(0, 0);
-  __syncthreads();
-  const int hin = a.in_centered ? Lin / 2 : 0;
-  for (int e = tid; e < nlines * Lin; e += nt) {
-    int b, j;
-    if (ax == 2) { b = e / Lin; j = e % Lin; }
-    else { j = e / nlines; b = e % nlines; }
-    cx<T> v = in[base_in + (int64_t)b * lstep_in + (int64_t)j * stride_in];
-    const int m = j - hin;  // mode number (node index when not centred)
-    if (a.in_phase != 0.0) {
-      double cyc = a.in_phase * (double)m;
-      cyc -= rint(cyc);
-      double s, c;
-      sincospi(2.0 * cyc, &s, &c);
-      v = v * mk<T>((T)c, (T)s);
+  // ---- line addressing
+  int64_t base_in, base_out, st_in, st_out;
+  bool live;
+  if (ax == 2) {
+    const int64_t lines = (int64_t)a.shape_in[0] * a.shape_in[1];
+    const int64_t l = (int64_t)blockIdx.x * B + b;
+    live = l < lines;
+    base_in = l * Lin;
+    base_out = l * Lout;
+    st_in = 1;
+    st_out = 1;
+  } else {
+    const int s2 = a.shape_in[2];
+    const int ptiles = (s2 + B - 1) / B;
+    const int o = blockIdx.x / ptiles, p = (blockIdx.x % ptiles) * B + b;
+    live = p < s2;
+    if (ax == 0) {
+      base_in = (int64_t)o * s2 + p;
+      base_out = (int64_t)o * a.shape_out[2] + p;
+      st_in = (int64_t)a.shape_in[1] * s2;
+      st_out = (int64_t)a.shape_out[1] * a.shape_out[2];
+    } else {
+      base_in = (int64_t)o * a.shape_in[1] * s2 + p;
+      base_out = (int64_t)o * a.shape_out[1] * a.shape_out[2] + p;
+      st_in = s2;
+      st_out = a.shape_out[2];
     }
-    const int pos = a.in_centered ? ((m % N) + N) % N : j;
-    buf0[b * ld + pos] = v;
-  }
-  __syncthreads();
-
-  // radix-2 Stockham: span Ns = 1, 2, ..., N/2
-  cx<T>* x = buf0;
-  cx<T>* y = buf1;
-  for (int Ns = 1; Ns < N; Ns <<= 1) {
-    const int tstep = N / (2 * Ns);
-    for (int e = tid; e < B * half; e += nt) {
-      const int b = e / half, j = e % half;
-      const int k = j & (Ns - 1);
-      const cx<T> t = tw[k * tstep];
-      const cx<T> u = x[b * ld + j];
-      const cx<T> v = x[b * ld + j + half] * t;
-      const int idx = ((j - k) << 1) + k;
-      y[b * ld + idx] = u + v;
-      y[b * ld + idx + Ns] = u - v;
-    }
-    __syncthreads();
-    cx<T>* tmp = x;
-    x = y;
-    y = tmp;
   }
 
-  const int hout = a.out_centered ? Lout / 2 : 0;
-  for (int e = tid; e < nlines * Lout; e += nt) {
-    int b, j;
-    if (ax == 2) { b = e / Lout; j = e % Lout; }
-    else { j = e / nlines; b = e % nlines; }
-    const int m = j - hout;
-    const int pos = a.out_centered ? ((m % N) + N) % N : j;
-    cx<T> v = x[b * ld + pos];
-    double cyc = a.out_phase * (double)m;
-    cyc -= rint(cyc);
-    double s, c;
-    sincospi(2.0 * cyc, &s, &c);
-    v = v * mk<T>((T)(c * a.scale), (T)(s * a.scale));
-    out[base_out + (int64_t)b * lstep_out + (int64_t)j * stride_out] = v;
+  // ---- first stage input: positions pos = j + r * (N / PT) of the line
+  cx<T> v[PT];
+  const int hin = Lin / 2;
+#pragma unroll
+  for (int r = 0; r < PT; ++r) {
+    const int pos = j + r * TPL;
+    int src, m;
+    if (a.in_centered) {
+      m = pos < N / 2 ? pos : pos - N;  // mode at this FFT position
+      src = m + hin;
+      if (src < 0 || src >= Lin) src = -1;
+    } else {
+      m = pos;
+      src = pos;
+    }
+    cx<T> x = mk<T>(0, 0);
+    if (live && src >= 0) {
+      x = in[base_in + (int64_t)src * st_in];
+      if (a.in_phase_kind) x = x * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
+    }
+    v[r] = x;
+  }
+
+  // ---- transform (natural-order result in the line buffer)
+  cx<T>* line = buf + b * LD;
+  fft_line<T, N>(v, line, j, tw, a.sign);
+
+  // ---- output: positions pos = j + r * TPL
+  const int hout = Lout / 2;
+#pragma unroll
+  for (int r = 0; r < PT; ++r) {
+    const int pos = j + r * TPL;
+    int dst, m;
+    if (a.out_centered) {
+      m = pos < N / 2 ? pos : pos - N;
+      dst = m + hout;
+      if (dst < 0 || dst >= Lout) continue;
+    } else {
+      m = pos;
+      dst = pos;
+    }
+    if (!live) continue;
+    cx<T> y = line[sidx<T>(pos)];
+    y = mk<T>(y.re * (T)a.scale, y.im * (T)a.scale);
+    if (a.out_phase_kind) y = y * phase_factor<T>(a.out_phase_kind, a.out_phase, m);
+    out[base_out + (int64_t)dst * st_out] = y;
   }
 }
 
 template <typename T>
-cudaError_t launch_fft_pass(FftArgs a, cudaStream_t st) {
-  const int N = a.N;
-  // lines per CTA: keep two ping-pong buffers + twiddles within ~96 KB
-  int B = (int)(96 * 1024 / (2 * (N + 1) * sizeof(cx<T>)));
-  if (B > 32) B = 32;
-  if (B < 1) B = 1;
-  if (a.axis != 2 && B > a.shape_in[2]) B = a.shape_in[2];
-  a.B = B;
-  size_t smem = (size_t)(2 * B * (N + 1) + N / 2) * sizeof(cx<T>);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(fft_lines_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
+__global__ void twiddle_kernel(cx<T>* tw, int n, int sign) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi((double)sign * 2.0 * (double)m / (double)n, &s, &c);
+    tw[m] = mk<T>((T)c, (T)s);
   }
+}
+
+std::mutex g_tw_mu;
+std::map<std::tuple<int, int, int, int>, void*> g_tw;  // (device, precision, n, sign) -> table
+
+}  // namespace
+
+const void* twiddles(int precision, int n, int sign, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto key = std::make_tuple(dev, precision, n, sign);
+  auto it = g_tw.find(key);
+  if (it != g_tw.end()) return it->second;
+  void* p = nullptr;
+  size_t bytes = (size_t)n * (precision == 64 ? 16 : 8);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  if (precision == 64) twiddle_kernel<double><<<(n + 255) / 256, 256, 0, st>>>((cx<double>*)p, n, sign);
+  else twiddle_kernel<float><<<(n + 255) / 256, 256, 0, st>>>((cx<float>*)p, n, sign);
+  cudaStreamSynchronize(st);
+  g_tw[key] = p;
+  return p;
+}
+
+namespace {
+
+template <typename T, int N, int B>
+cudaError_t launch_nb(const FftArgs& a, cudaStream_t st) {
+  constexpr int TPL = N >= 8 ? N / 8 : 1;
   int64_t blocks;
-  if (a.axis == 2) {
-    blocks = ceil_div((int64_t)a.shape_in[0] * a.shape_in[1], B);
-  } else {
+  if (a.axis == 2) blocks = ceil_div((int64_t)a.shape_in[0] * a.shape_in[1], B);
+  else {
     const int so = a.axis == 0 ? a.shape_in[1] : a.shape_in[0];
     blocks = (int64_t)so * ceil_div(a.shape_in[2], B);
   }
-  fft_lines_kernel<T><<<(unsigned)blocks, 256, smem, st>>>(a);
+  constexpr size_t smem = sizeof(cx<T>) * B * LineLD<T, N>::value;
+  if (smem > 48 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(fft_kernel<T, N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+  }
+  fft_kernel<T, N, B><<<(unsigned)blocks, B * TPL, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+// lines per CTA: strided axes need >= 128 contiguous bytes per row per CTA
+// (B = 16 complex64 / 8 complex128) for full-sector, full-line coalescing;
+// the contiguous axis only needs enough threads (B * N / 8 >= 256).
+template <typename T, int N>
+cudaError_t launch_n(const FftArgs& a, cudaStream_t st) {
+  constexpr int TPL = N >= 8 ? N / 8 : 1;
+  constexpr int B_row = 128 / sizeof(cx<T>);
+  constexpr int B_thr = (256 / TPL) < 1 ? 1 : (256 / TPL) > 32 ? 32 : (256 / TPL);
+  constexpr int B_str = (B_row > B_thr ? B_row : B_thr) * TPL > 1024 ? 1024 / TPL : (B_row > B_thr ? B_row : B_thr);
+  if (a.axis == 2) return launch_nb<T, N, B_thr>(a, st);
+  return launch_nb<T, N, B_str>(a, st);
+}
+
+template <typename T>
+cudaError_t launch_fft(const FftArgs& a, int n, cudaStream_t st) {
+  switch (n) {
+    case 2: return launch_n<T, 2>(a, st);
+    case 4: return launch_n<T, 4>(a, st);
+    case 8: return launch_n<T, 8>(a, st);
+    case 16: return launch_n<T, 16>(a, st);
+    case 32: return launch_n<T, 32>(a, st);
+    case 64: return launch_n<T, 64>(a, st);
+    case 128: return launch_n<T, 128>(a, st);
+    case 256: return launch_n<T, 256>(a, st);
+    case 512: return launch_n<T, 512>(a, st);
+    case 1024: return launch_n<T, 1024>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int phase_kind(double ph) {
+  double f = ph - floor(ph);
+  if (f == 0.0) return 0;
+  if (f == 0.5) return 1;
+  return 2;
 }
 
 }  // namespace
@@ -201,7 +248,7 @@ extern "C" int gf_fft_pass(int precision, const void* in, void* out, const int32
                            double in_phase, double out_phase, double scale, void* stream) {
   GF_CHECK(in && out && shape_in && shape_out, GF_EINVAL, "null argument");
   GF_CHECK(axis >= 0 && axis < 3, GF_EINVAL, "axis must be 0, 1 or 2");
-  GF_CHECK(n >= 2 && n <= 4096 && (n & (n - 1)) == 0, GF_EINVAL, "FFT length must be a power of two in [2, 4096]");
+  GF_CHECK(n >= 2 && n <= 1024 && (n & (n - 1)) == 0, GF_EINVAL, "FFT length must be a power of two in [2, 1024]");
   GF_CHECK(sign == -1 || sign == 1, GF_EINVAL, "sign must be -1 or +1");
   GF_CHECK(precision == 32 || precision == 64, GF_EINVAL, "precision must be 32 or 64");
   for (int a = 0; a < 3; ++a)
@@ -209,23 +256,26 @@ extern "C" int gf_fft_pass(int precision, const void* in, void* out, const int32
   GF_CHECK(shape_in[axis] <= n && shape_out[axis] <= n, GF_EINVAL, "line longer than the FFT length");
   GF_CHECK(in_centered || shape_in[axis] == n, GF_EINVAL, "node-ordered input must have length n");
   GF_CHECK(out_centered || shape_out[axis] == n, GF_EINVAL, "node-ordered output must have length n");
+  cudaStream_t st = (cudaStream_t)stream;
   FftArgs a = {};
   a.in = in;
   a.out = out;
+  a.tw = twiddles(precision, n, sign, st);
+  GF_CHECK(a.tw != nullptr, GF_ENOMEM, "twiddle table allocation failed");
   for (int k = 0; k < 3; ++k) {
     a.shape_in[k] = shape_in[k];
     a.shape_out[k] = shape_out[k];
   }
   a.axis = axis;
-  a.N = n;
   a.in_centered = in_centered;
   a.out_centered = out_centered;
   a.sign = sign;
   a.in_phase = in_phase;
   a.out_phase = out_phase;
+  a.in_phase_kind = phase_kind(in_phase);
+  a.out_phase_kind = phase_kind(out_phase);
   a.scale = scale;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (precision == 64) GF_CUDA(launch_fft_pass<double>(a, st));
-  else GF_CUDA(launch_fft_pass<float>(a, st));
+  if (precision == 64) GF_CUDA(launch_fft<double>(a, n, st));
+  else GF_CUDA(launch_fft<float>(a, n, st));
   return 0;
 }
