@@ -168,6 +168,9 @@ int gf_measure_launch(int n, int blocks, double *host_us, double *dev_us);
  * per thread (0 = auto). */
 int gf_set_cascade_variant(int variant);
 int gf_set_cascade_tile(int tile);
+/* Debug: per-CTA phase timestamps (globaltimer ns) of the single-query kernel
+ * into a device buffer of >= 8 x blocks uint64 (NULL disables). */
+int gf_set_cascade_debug(void *dev_buf);
 int gf_set_cascade_run_length(int L);
 
 #ifdef __cplusplus

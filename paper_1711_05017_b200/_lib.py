@@ -31,6 +31,9 @@ SIGNATURES = {
     "gf_window_device_ptr": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
     "gf_cascade": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double,
                                   c_dp, c_dp, c_dp, ctypes.c_int, c_dp]),
+    # same symbol bound with void* arguments for the per-query fast path
+    "gf_cascade_fast": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_vp, ctypes.c_double,
+                                       c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
     "gf_cascade_batch": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double,
                                         c_dp, ctypes.c_int, ctypes.c_int64, c_vp, c_vp, c_vp]),
     "gf_cascade_serial": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double,
@@ -58,8 +61,13 @@ SIGNATURES = {
                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
     "gf_score_field": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_i32p, c_dp, c_dp,
                                       ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
+    "gf_set_cascade_debug": (ctypes.c_int, [c_vp]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),
 }
+
+
+# extra Python-side bindings of an exported symbol (name -> symbol)
+ALIASES = {"gf_cascade_fast": "gf_cascade"}
 
 
 def _load():
@@ -70,9 +78,14 @@ def _load():
         )
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if name in ALIASES:
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    for alias, target in ALIASES.items():
+        fn = ctypes.CFUNCTYPE(SIGNATURES[alias][0], *SIGNATURES[alias][1])((target, lib))
+        setattr(lib, alias, fn)
     return lib
 
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -151,22 +152,44 @@ def as_device_window(C):
 # cascade (Q1) and batched sweep (Q3)
 
 
+class _QueryBuffers(threading.local):
+    """Per-thread pinned-by-address host buffers for the single-query path
+    (no per-call array allocation or ctypes pointer construction)."""
+
+    def __init__(self):
+        self.arg = np.zeros(24)   # R (9) | t_eff (3) | center (3) | domega (3)
+        self.out = np.zeros(14)
+        a = self.arg.ctypes.data
+        self.pR, self.pt, self.pc, self.pd = (ctypes.c_void_p(a), ctypes.c_void_p(a + 72),
+                                              ctypes.c_void_p(a + 96), ctypes.c_void_p(a + 120))
+        self.pout = ctypes.c_void_p(self.out.ctypes.data)
+
+
+_qb = _QueryBuffers()
+
+
 def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
     """Score + gradients over one retained-mode window (backend.py:153-164).
 
     Returns complex128[1 + d + n_rot]: [score, dS/dt..., dS/dtheta...], times
     dcell, computed by the CUDA cascade kernel.
     """
-    W1, W2 = as_device_window(C1), as_device_window(C2)
+    W1 = C1 if type(C1) is DeviceWindow else as_device_window(C1)
+    W2 = C2 if type(C2) is DeviceWindow else as_device_window(C2)
     d = W1.ndim
-    R = np.ascontiguousarray(R, dtype=np.float64)
-    t_eff = np.ascontiguousarray(t_eff, dtype=np.float64)
-    center = np.ascontiguousarray(center, dtype=np.float64)
-    dom = np.ascontiguousarray(domega, dtype=np.float64)
-    out = np.empty(7 if d == 3 else 4, dtype=np.complex128)
-    check(LIB.gf_cascade(W1.handle, W2.handle, int(bool(wrap)), dptr(dom), float(dcell), dptr(R), dptr(t_eff),
-                         dptr(center), _prec_bits(precision), dptr(out.view(np.float64))))
-    return out
+    q = _qb
+    arg = q.arg
+    Rf = np.asarray(R, dtype=np.float64).reshape(-1)
+    arg[: d * d] = Rf
+    arg[9: 9 + d] = t_eff
+    arg[12: 12 + d] = center
+    arg[15: 15 + d] = domega
+    rc = LIB.gf_cascade_fast(W1.handle, W2.handle, 1 if wrap else 0, q.pd, float(dcell), q.pR, q.pt, q.pc,
+                             64 if (precision or _precision) == "fp64" else 32, q.pout)
+    if rc:
+        check(rc)
+    n = 14 if d == 3 else 8
+    return q.out[:n].copy().view(np.complex128)
 
 
 def pack_poses(R, t_eff):

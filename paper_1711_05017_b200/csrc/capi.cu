@@ -8,6 +8,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -55,7 +57,14 @@ static Window* find_window(uint64_t h) {
 struct Context {
   int device = -1;
   cudaStream_t stream = nullptr;
-  double* host_out = nullptr;     // pinned + mapped, 14 doubles
+  double* host_out = nullptr;     // pinned + mapped: 14 doubles, then the completion word at [16]
+  unsigned long long seq = 0;
+  // cached launch arguments of the last single query (same windows/grid)
+  bool cached = false;
+  uint64_t ch1 = 0, ch2 = 0;
+  int cwrap = -1, cprec = 0;
+  double cdom[3] = {0, 0, 0}, cdcell = 0, ccen[3] = {0, 0, 0};
+  CascadeArgs cargs;
   double* dev_out_alias = nullptr;
   double* partials = nullptr;
   unsigned* counters = nullptr;
@@ -65,6 +74,7 @@ static thread_local Context tl_ctx;
 static int g_run_length = 0;
 static int g_variant = 1;
 static int g_tile = 0;
+static unsigned long long* g_debug = nullptr;
 
 static int ensure_context() {
   int dev = 0;
@@ -173,6 +183,7 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
   a.seg_len = g_run_length;
   a.variant = g_variant;
   a.tile_force = g_tile;
+  a.debug = g_debug;
   return 0;
 }
 
@@ -252,6 +263,7 @@ int gf_window_create_device(const void* dev_c128, int d, const int32_t* w, uint6
 }
 
 int gf_window_destroy(uint64_t handle) {
+  if (tl_ctx.ch1 == handle || tl_ctx.ch2 == handle) tl_ctx.cached = false;
   std::unique_ptr<Window> victim;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -276,6 +288,13 @@ int gf_set_cascade_variant(int v) {
   return 0;
 }
 
+// Debug: per-block phase timestamps of the single-query kernel (device
+// buffer of >= 8 * blocks uint64, or null to disable).
+int gf_set_cascade_debug(void* dev_buf) {
+  g_debug = (unsigned long long*)dev_buf;
+  return 0;
+}
+
 int gf_set_cascade_tile(int ts) {
   GF_CHECK(ts == 0 || ts == 8 || ts == 16, GF_EINVAL, "tile must be 0 (auto), 8 or 16");
   g_tile = ts;
@@ -296,20 +315,57 @@ int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double 
   Context& c = tl_ctx;
   Window* w1 = find_window(h1);
   Window* w2 = find_window(h2);
-  CascadeArgs a;
-  rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, c.stream);
-  if (rc) return rc;
-  embed_pose(w1->d, R, t_eff, a.pose_inline);
-  a.poses = nullptr;
-  plan_cascade(a, 1, 2 * 148);
-  rc = ensure_scratch(c, (int64_t)a.blocks_per_pose * kNumMoments, 1, c.stream);
-  if (rc) return rc;
-  a.partials = c.partials;
-  a.counters = c.counters;
-  a.out = c.dev_out_alias;
+  GF_CHECK(w1 && w2, GF_EINVAL, "unknown window handle");
+  const int d = w1->d;
+  // the haptic loop queries the same window pair at the same grid every
+  // frame: reuse the planned launch, only the pose changes
+  const bool hit = c.cached && c.ch1 == h1 && c.ch2 == h2 && c.cwrap == (wrap ? 1 : 0) && c.cprec == precision &&
+                   c.cdcell == dcell && std::memcmp(c.cdom, domega, d * sizeof(double)) == 0 &&
+                   std::memcmp(c.ccen, center, d * sizeof(double)) == 0 && g_debug == c.cargs.debug;
+  if (!hit) {
+    CascadeArgs a;
+    rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, c.stream);
+    if (rc) return rc;
+    a.poses = nullptr;
+    plan_cascade(a, 1, 2 * 148);
+    rc = ensure_scratch(c, (int64_t)a.blocks_per_pose * kNumMoments, 1, c.stream);
+    if (rc) return rc;
+    a.partials = c.partials;
+    a.counters = c.counters;
+    a.out = c.dev_out_alias;
+    a.done_flag = a.single ? reinterpret_cast<volatile unsigned long long*>(c.dev_out_alias + 16) : nullptr;
+    c.cargs = a;
+    c.ch1 = h1;
+    c.ch2 = h2;
+    c.cwrap = wrap ? 1 : 0;
+    c.cprec = precision;
+    c.cdcell = dcell;
+    std::memcpy(c.cdom, domega, d * sizeof(double));
+    std::memcpy(c.ccen, center, d * sizeof(double));
+    c.cached = true;
+  }
+  CascadeArgs& a = c.cargs;
+  embed_pose(d, R, t_eff, a.pose_inline);
+  a.done_seq = ++c.seq;
   GF_CUDA(launch_cascade(a, 1, c.stream));
-  GF_CUDA(cudaStreamSynchronize(c.stream));
-  if (w1->d == 3) {
+  if (a.done_flag) {
+    // poll the mapped completion word (no driver call on the fast path);
+    // fall back to a stream sync after ~1 s so a failed kernel surfaces
+    volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c.host_out + 16);
+    auto t0 = std::chrono::steady_clock::now();
+    unsigned spins = 0;
+    while (*flag != a.done_seq) {
+      if ((++spins & 0xffff) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1)) {
+        GF_CUDA(cudaStreamSynchronize(c.stream));
+        GF_CHECK(*flag == a.done_seq, GF_EINTERNAL, "query kernel finished without publishing its result");
+        break;
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  } else {
+    GF_CUDA(cudaStreamSynchronize(c.stream));
+  }
+  if (d == 3) {
     std::memcpy(out, c.host_out, 14 * sizeof(double));
   } else {  // [S, Tx, Ty, Gz]
     std::memcpy(out, c.host_out, 6 * sizeof(double));

@@ -38,6 +38,9 @@ struct CascadeArgs {
   double* partials;      // n_poses * blocks_per_pose * kNumMoments (if bpp > 1)
   unsigned* counters;    // n_poses, zero-initialised, re-armed by the kernel
   double* out;           // n_poses * 14 (interleaved complex128 x 7)
+  unsigned long long* debug;  // optional per-block phase timestamps (single kernel)
+  volatile unsigned long long* done_flag;  // single kernel: host-mapped completion word (or null)
+  unsigned long long done_seq;            // value stored there after the outputs
 };
 
 // 26 moment accumulators (layout = the moment index order used by finalize)

@@ -18,6 +18,9 @@
 #include "cascade.cuh"
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+#include <cuda/atomic>
+
 #include <math.h>
 #include <stdlib.h>
 
@@ -25,12 +28,17 @@ namespace gf {
 namespace {
 
 constexpr int kThreads = 256;
+int g_cluster = 2;  // CTAs per cluster (DSMEM reduction stage); 1 disables
 
 struct SinglePose {
   double mu[3][3];
   double R[9];
   double targ[3];
   int p, q, r, nP, nQ;
+  // finalize coefficients (computed during setup, used by the last block):
+  double cg[3][3][3];  // G_g += cg[g][b][a] * Y[b][a]  (= -A_g[a][b] dw_a / dw_b)
+  double kq[3][3];     // G_g += 2 pi i kq[g][a] Z_a     (= dw_a q_g[a])
+  double kt[3];        // T_a  = 2 pi i kt[a] Z_a        (= dw_a)
 };
 
 __device__ __forceinline__ double exact_u_s(const double* R, const double* dom, int a, int kx, int ky, int kz,
@@ -43,31 +51,25 @@ __device__ __forceinline__ double exact_u_s(const double* R, const double* dom, 
 }
 
 // Output slot i (0..13, interleaved complex) as a linear form of the 26
-// moments; called by 14 threads in parallel.
-__device__ __forceinline__ double finalize_slot(const CascadeArgs& a, const double* R, const double* m, int i) {
+// moments, from the coefficients precomputed in setup (14 threads).
+__device__ __forceinline__ double finalize_slot(const CascadeArgs& a, const SinglePose& sp, const double* m, int i) {
   const double TWO_PI = 6.283185307179586;
   const double dc = a.dcell;
   if (i < 2) return dc * m[i];
   if (i < 8) {  // T_a = 2 pi i dw_a Z_a
-    int ax = (i - 2) >> 1;
-    double k = dc * TWO_PI * a.dom[ax];
+    const int ax = (i - 2) >> 1;
+    const double k = dc * TWO_PI * sp.kt[ax];
     return (i & 1) ? k * m[2 + 2 * ax] : -k * m[3 + 2 * ax];
   }
   const int g = (i - 8) >> 1, im = i & 1;
-  // A_g = Omega_g R: rows (generator g) -- see _core.pyx:615-626
-  double A[3][3];
-  for (int b = 0; b < 3; ++b) {
-    double r0 = R[b], r1 = R[3 + b], r2 = R[6 + b];
-    if (g == 0) { A[0][b] = 0.0; A[1][b] = -r2; A[2][b] = r1; }
-    else if (g == 1) { A[0][b] = r2; A[1][b] = 0.0; A[2][b] = -r0; }
-    else { A[0][b] = -r1; A[1][b] = r0; A[2][b] = 0.0; }
-  }
   double acc = 0.0;
-  for (int b = 0; b < 3; ++b)
-    for (int ax = 0; ax < 3; ++ax) acc += -A[ax][b] * (a.dom[ax] / a.dom[b]) * m[8 + im + 2 * (3 * b + ax)];
+#pragma unroll
+  for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) acc += sp.cg[g][bb][ax] * m[8 + im + 2 * (3 * bb + ax)];
+#pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
-    double q = A[ax][0] * a.center[0] + A[ax][1] * a.center[1] + A[ax][2] * a.center[2];
-    double k = TWO_PI * a.dom[ax] * q;
+    const double k = TWO_PI * sp.kq[g][ax];
     acc += im ? k * m[2 + 2 * ax] : -k * m[3 + 2 * ax];
   }
   return dc * acc;
@@ -85,6 +87,14 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   __shared__ unsigned ticket;
 
   const int tid = threadIdx.x;
+  unsigned long long* dbg = a.debug ? a.debug + (int64_t)blockIdx.x * 8 : nullptr;
+#define GF_STAMP(k)                                                                 \
+  if (dbg && tid == 0) {                                                           \
+    unsigned long long t_;                                                         \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+    dbg[k] = t_;                                                                   \
+  }
+  GF_STAMP(0)
   const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
   const double* src = a.poses ? a.poses + a.pose_offset * 12 : a.pose_inline;
@@ -94,6 +104,29 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
     sp.mu[ia][ib] = -src[ib * 3 + ia] * (a.dom[ib] / a.dom[ia]);
   }
   if (tid >= 16 && tid < 19) sp.targ[tid - 16] = a.dom[tid - 16] * src[9 + tid - 16];
+  if (tid >= 32 && tid < 32 + 27) {  // A_g = Omega_g R (_core.pyx:615-626)
+    const int k = tid - 32, g = k / 9, bb = (k / 3) % 3, ax = k % 3;
+    const double* Rr = src;  // row-major R
+    double Aab;  // A_g[ax][bb]
+    if (g == 0) Aab = ax == 0 ? 0.0 : (ax == 1 ? -Rr[6 + bb] : Rr[3 + bb]);
+    else if (g == 1) Aab = ax == 0 ? Rr[6 + bb] : (ax == 1 ? 0.0 : -Rr[bb]);
+    else Aab = ax == 0 ? -Rr[3 + bb] : (ax == 1 ? Rr[bb] : 0.0);
+    sp.cg[g][bb][ax] = -Aab * (a.dom[ax] / a.dom[bb]);
+  }
+  if (tid >= 64 && tid < 64 + 9) {  // q_g = A_g c
+    const int g = (tid - 64) / 3, ax = (tid - 64) % 3;
+    const double* Rr = src;
+    double q = 0.0;
+    for (int bb = 0; bb < 3; ++bb) {
+      double Aab;
+      if (g == 0) Aab = ax == 0 ? 0.0 : (ax == 1 ? -Rr[6 + bb] : Rr[3 + bb]);
+      else if (g == 1) Aab = ax == 0 ? Rr[6 + bb] : (ax == 1 ? 0.0 : -Rr[bb]);
+      else Aab = ax == 0 ? -Rr[3 + bb] : (ax == 1 ? Rr[bb] : 0.0);
+      q += Aab * a.center[bb];
+    }
+    sp.kq[g][ax] = a.dom[ax] * q;
+  }
+  if (tid >= 96 && tid < 99) sp.kt[tid - 96] = a.dom[tid - 96];
   __syncthreads();
   if (tid == 0) {
     int r = 2;
@@ -144,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
 
   Acc26<T> acc;
   acc.zero();
+  GF_STAMP(1)
   for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
     const int kr = unit % wr;
     const int iq = (unit / wr) % sp.nQ;
@@ -206,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
     acc.add(bV, base * dU, base * dV, base * dS, kapx, kapy, kapz);
   }
 
+  GF_STAMP(2)
   // ---- block reduction through a shared-memory transpose (fixed order)
 #pragma unroll
   for (int c = 0; c < kNumMoments; ++c) tr[c][tid] = acc.v[c];
@@ -214,10 +249,15 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   double part = 0.0;
   const int c = tid >> 3, s = tid & 7;
   if (c < kNumMoments) {
-    T acc2 = (T)0;
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) acc2 += tr[c][s * 32 + i];
-    part = (double)acc2;
+    T q0 = (T)0, q1 = (T)0, q2 = (T)0, q3 = (T)0;  // 4 independent chains, fixed order
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      q0 += tr[c][s * 32 + i];
+      q1 += tr[c][s * 32 + i + 1];
+      q2 += tr[c][s * 32 + i + 2];
+      q3 += tr[c][s * 32 + i + 3];
+    }
+    part = (double)((q0 + q1) + (q2 + q3));
   }
   // combine the 8 segments of each moment (lanes 8 apart inside one warp)
 #pragma unroll
@@ -228,43 +268,60 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   double* out = a.out;
   const int bpp = gridDim.x;
   if (bpp == 1) {
-    if (tid < 14) out[tid] = finalize_slot(a, sp.R, red, tid);
+    if (tid < 14) out[tid] = finalize_slot(a, sp, red, tid);
     return;
   }
-  double* pt = a.partials + (int64_t)blockIdx.x * kNumMoments;
-  if (tid < kNumMoments) pt[tid] = red[tid];
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) ticket = atomicAdd(a.counters, 1u);
-  __syncthreads();
-  if (ticket != (unsigned)(bpp - 1)) return;
-  __threadfence();
-  // last block: 26 moments x 9 segments; each thread streams its segment's
-  // partials with independent loads (fixed order), then segments combine
-  if (tid < kNumMoments * 9) {
-    const int cc = tid / 9, sg = tid % 9;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int b = sg;
-    for (; b + 27 < bpp; b += 36) {
-      v0 += __ldcg(a.partials + (int64_t)b * kNumMoments + cc);
-      v1 += __ldcg(a.partials + (int64_t)(b + 9) * kNumMoments + cc);
-      v2 += __ldcg(a.partials + (int64_t)(b + 18) * kNumMoments + cc);
-      v3 += __ldcg(a.partials + (int64_t)(b + 27) * kNumMoments + cc);
-    }
-    for (; b < bpp; b += 9) v0 += __ldcg(a.partials + (int64_t)b * kNumMoments + cc);
-    reinterpret_cast<double*>(&tr[0][0])[tid] = (v0 + v1) + (v2 + v3);
-  }
-  __syncthreads();
-  if (tid < kNumMoments) {
-    const double* seg = reinterpret_cast<const double*>(&tr[0][0]) + tid * 9;
+  GF_STAMP(3)
+  // ---- cluster stage: rank 0 of each 8-CTA cluster sums its cluster's
+  // block moments through distributed shared memory (fixed rank order)
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned crank = cluster.block_rank(), csize = cluster.num_blocks();
+  const int cid = blockIdx.x / (int)csize, nclusters = gridDim.x / (int)csize;
+  cluster.sync();
+  if (crank == 0 && tid < kNumMoments) {
     double v = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) v += seg[k];
-    red[tid] = v;
+    for (unsigned r = 0; r < csize; ++r) v += cluster.map_shared_rank(red, r)[tid];
+    a.partials[(int64_t)tid * nclusters + cid] = v;  // moment-major
+  }
+  cluster.sync();  // keep the other ranks' shared memory alive until read
+  if (crank != 0) return;
+  // ---- grid stage: integer ticket with release/acquire ordering
+  __syncthreads();
+  if (tid == 0) {
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> ctr(*a.counters);
+    ticket = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
   }
   __syncthreads();
-  if (tid < 14) out[tid] = finalize_slot(a, sp.R, red, tid);
+  GF_STAMP(4)
+  if (ticket != (unsigned)(nclusters - 1)) return;
+  // last leader: 26 moments x 8 segments, independent loads, fixed order
+  double part2 = 0.0;
+  if (c < kNumMoments) {
+    const double* row = a.partials + (int64_t)c * nclusters;
+    double q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int b = s + 8 * i;
+      q[i] = b < nclusters ? __ldcg(row + b) : 0.0;
+    }
+    part2 = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    for (int b = s + 64; b < nclusters; b += 8) part2 += __ldcg(row + b);
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) part2 += __shfl_down_sync(0xffffffffu, part2, o, 8);
+  if (c < kNumMoments && s == 0) red[c] = part2;
+  __syncthreads();
+  if (tid < 14) out[tid] = finalize_slot(a, sp, red, tid);
   if (tid == 0) a.counters[0] = 0u;
+  if (a.done_flag) {  // publish completion to the polling host thread
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      *a.done_flag = a.done_seq;
+    }
+  }
+  GF_STAMP(5)
 }
 
 template <typename T, bool WRAP>
@@ -277,8 +334,19 @@ cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  cascade3d_single_kernel<T, WRAP><<<a.blocks_per_pose, kThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.blocks_per_pose);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = g_cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cascade3d_single_kernel<T, WRAP>, a);
 }
 
 }  // namespace
@@ -291,9 +359,12 @@ int single_blocks(const CascadeArgs& a, int sms) {
     int64_t u = ceil_div(a.w[o1], 16) * ceil_div(a.w[o2], 16) * a.w[r];
     if (best == 0 || u < best) best = u;
   }
-  int64_t target = (int64_t)sms * (a.precision == 32 ? 3 : 2);
+  int64_t target = (int64_t)sms * 2;  // 2 CTAs per SM: one resident wave, measured best (profiles/r01_cascade_notes.md)
   if (const char* env = getenv("GF_SINGLE_BLOCKS")) target = atoi(env);  // experiments only
-  return (int)(best < target ? best : target);
+  int64_t b = best < target ? best : target;
+  if (const char* env = getenv("GF_SINGLE_CLUSTER")) g_cluster = atoi(env);  // experiments only
+  b = (b / g_cluster) * g_cluster;  // whole clusters
+  return (int)(b < g_cluster ? g_cluster : b);
 }
 
 cudaError_t launch_cascade_single(const CascadeArgs& a, cudaStream_t st) {

@@ -30,6 +30,8 @@ def test_header_symbols_exported_and_bound():
     for s in syms:
         getattr(lib, s)  # raises AttributeError if not exported
         assert s in _lib.SIGNATURES, f"{s} declared in the header but not bound in _lib"
+    for alias, target in _lib.ALIASES.items():
+        assert target in syms
 
 
 def test_library_reports_missing_device_loudly():
