@@ -361,7 +361,10 @@ int single_blocks(const CascadeArgs& a, int sms) {
   }
   int64_t target = (int64_t)sms * 2;  // 2 CTAs per SM: one resident wave, measured best (profiles/r01_cascade_notes.md)
   if (const char* env = getenv("GF_SINGLE_BLOCKS")) target = atoi(env);  // experiments only
+  // equal work per CTA: the largest count <= target that gives every CTA the
+  // same number of units (no straggler CTA with one extra unit)
   int64_t b = best < target ? best : target;
+  if (best > target) b = best / ceil_div(best, target);
   if (const char* env = getenv("GF_SINGLE_CLUSTER")) g_cluster = atoi(env);  // experiments only
   b = (b / g_cluster) * g_cluster;  // whole clusters
   return (int)(b < g_cluster ? g_cluster : b);
