@@ -39,6 +39,7 @@ struct SinglePose {
   double cg[3][3][3];  // G_g += cg[g][b][a] * Y[b][a]  (= -A_g[a][b] dw_a / dw_b)
   double kq[3][3];     // G_g += 2 pi i kq[g][a] Z_a     (= dw_a q_g[a])
   double kt[3];        // T_a  = 2 pi i kt[a] Z_a        (= dw_a)
+  long long ufix[3][4];  // fixed-point u_a = ufix[a][3] + sum_b ufix[a][b] kappa_b
 };
 
 __device__ __forceinline__ double exact_u_s(const double* R, const double* dom, int a, int kx, int ky, int kz,
@@ -127,6 +128,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
     sp.kq[g][ax] = a.dom[ax] * q;
   }
   if (tid >= 96 && tid < 99) sp.kt[tid - 96] = a.dom[tid - 96];
+  if (tid >= 128 && tid < 140) {
+    const int ia = (tid - 128) / 4, ib = (tid - 128) % 4;
+    sp.ufix[ia][ib] = ib == 3 ? to_fix32((double)(ia == 0 ? hx : (ia == 1 ? hy : hz)))
+                              : to_fix32(-src[ib * 3 + ia] * (a.dom[ib] / a.dom[ia]));
+  }
   __syncthreads();
   if (tid == 0) {
     int r = 2;
@@ -188,24 +194,50 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
     const int ky = p == 1 ? kp : (q == 1 ? kq : kr);
     const int kz = p == 2 ? kp : (q == 2 ? kq : kr);
     const T kapx = (T)(kx - hx), kapy = (T)(ky - hy), kapz = (T)(kz - hz);
-    T u[3] = {fma(m02, kapz, fma(m01, kapy, fma(m00, kapx, (T)hx))),
-              fma(m12, kapz, fma(m11, kapy, fma(m10, kapx, (T)hy))),
-              fma(m22, kapz, fma(m21, kapy, fma(m20, kapx, (T)hz)))};
     T fl[3], f[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      fl[ax] = floor(u[ax]);
-      f[ax] = u[ax] - fl[ax];
-    }
-    const bool tz = a.dim == 3 && (f[2] < eps || f[2] > (T)1 - eps);
-    if (f[0] < eps || f[0] > (T)1 - eps || f[1] < eps || f[1] > (T)1 - eps || tz) {
+    if constexpr (sizeof(T) == 4) {
+      // exact 32.32 fixed-point index; float64 reference order only within 1e-6 of an integer
+      unsigned lo[3];
+      const int kk[3] = {kx - hx, ky - hy, kz - hz};
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
-        if ((ax < 2 || tz) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
-          double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
-          double fe = floor(ue);
-          fl[ax] = (T)fe;
-          f[ax] = (T)(ue - fe);
+        const long long u = sp.ufix[ax][3] + (long long)kk[0] * sp.ufix[ax][0] + (long long)kk[1] * sp.ufix[ax][1] +
+                            (long long)kk[2] * sp.ufix[ax][2];
+        lo[ax] = fix_lo(u);
+        fl[ax] = (T)fix_floor(u);
+        f[ax] = fix_frac(lo[ax]);
+      }
+      const bool tz = a.dim == 3 && fix_tie(lo[2]);
+      if (fix_tie(lo[0]) || fix_tie(lo[1]) || tz) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          if ((ax < 2 || tz) && fix_tie(lo[ax])) {
+            double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+            double fe = floor(ue);
+            fl[ax] = (T)fe;
+            f[ax] = (T)(ue - fe);
+          }
+        }
+      }
+    } else {
+      T u[3] = {fma(m02, kapz, fma(m01, kapy, fma(m00, kapx, (T)hx))),
+                fma(m12, kapz, fma(m11, kapy, fma(m10, kapx, (T)hy))),
+                fma(m22, kapz, fma(m21, kapy, fma(m20, kapx, (T)hz)))};
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        fl[ax] = floor(u[ax]);
+        f[ax] = u[ax] - fl[ax];
+      }
+      const bool tz = a.dim == 3 && (f[2] < eps || f[2] > (T)1 - eps);
+      if (f[0] < eps || f[0] > (T)1 - eps || f[1] < eps || f[1] > (T)1 - eps || tz) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          if ((ax < 2 || tz) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
+            double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+            double fe = floor(ue);
+            fl[ax] = (T)fe;
+            f[ax] = (T)(ue - fe);
+          }
         }
       }
     }

@@ -84,6 +84,24 @@ __device__ __forceinline__ double4 ldg_pair(const double4* p) {
   return make_double4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// ---------------------------------------------------------------------------
+// 32.32 fixed-point continuous window index (fp32 engine).
+//
+// u = h + sum_b mu[a][b] kappa_b is formed exactly in int64 from fixed-point
+// coefficients (|error| < 1e-7 for windows up to 1024), so floor(u) comes
+// from a shift and frac(u) from the low word, with no float rounding of a
+// large |u| -- the near-integer band that must be re-decided in float64
+// reference order shrinks from ~1e-4 to 1e-6 and the conversion pipe is not
+// used.  Non-negative and negative u both floor correctly (arithmetic shift).
+__host__ __device__ __forceinline__ long long to_fix32(double x) {
+  return (long long)llrint(x * 4294967296.0);
+}
+constexpr unsigned kFixTieEps = 4295u;  // 1e-6 in units of 2^-32
+__device__ __forceinline__ int fix_floor(long long u) { return (int)(u >> 32); }
+__device__ __forceinline__ unsigned fix_lo(long long u) { return (unsigned)((unsigned long long)u & 0xffffffffull); }
+__device__ __forceinline__ float fix_frac(unsigned lo) { return __uint_as_float(0x3f800000u | (lo >> 9)) - 1.0f; }
+__device__ __forceinline__ bool fix_tie(unsigned lo) { return lo < kFixTieEps || lo > 0xffffffffu - kFixTieEps; }
+
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace gf
