@@ -163,6 +163,16 @@ int gf_measure_fma_peak(int precision, double *tflops);
 /* Launch-overhead probe: host and device microseconds per empty launch. */
 int gf_measure_launch(int n, int blocks, double *host_us, double *dev_us);
 
+/* Persistent haptic server (Q1 latency path): a resident grid serves one
+ * query per call through a host-mapped mailbox -- no kernel launch per
+ * query.  Same window pair / grid for the server's lifetime; the kernel exits
+ * after idle_timeout_s without requests (<= 0: 30 s) or on gf_server_stop.
+ * gf_server_query has gf_cascade's pose and output conventions. */
+int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double *domega, double dcell, const double *center,
+                    int precision, double idle_timeout_s, uint64_t *server_id);
+int gf_server_query(uint64_t server_id, const double *R, const double *t_eff, double *out);
+int gf_server_stop(uint64_t server_id);
+
 /* Tuning knobs for experiments: kernel variant (0 = u-space tiled, the
  * default; 1 = direct gather) and the direct variant's run length along kz
  * per thread (0 = auto). */

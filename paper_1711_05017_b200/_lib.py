@@ -62,12 +62,17 @@ SIGNATURES = {
     "gf_score_field": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_i32p, c_dp, c_dp,
                                       ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
     "gf_set_cascade_debug": (ctypes.c_int, [c_vp]),
+    "gf_server_start": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double, c_dp,
+                                       ctypes.c_int, ctypes.c_double, c_u64p]),
+    "gf_server_query": (ctypes.c_int, [ctypes.c_uint64, c_dp, c_dp, c_dp]),
+    "gf_server_query_fast": (ctypes.c_int, [ctypes.c_uint64, c_vp, c_vp, c_vp]),
+    "gf_server_stop": (ctypes.c_int, [ctypes.c_uint64]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),
 }
 
 
 # extra Python-side bindings of an exported symbol (name -> symbol)
-ALIASES = {"gf_cascade_fast": "gf_cascade"}
+ALIASES = {"gf_cascade_fast": "gf_cascade", "gf_server_query_fast": "gf_server_query"}
 
 
 def _load():

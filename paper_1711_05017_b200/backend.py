@@ -184,12 +184,70 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
     arg[9: 9 + d] = t_eff
     arg[12: 12 + d] = center
     arg[15: 15 + d] = domega
-    rc = LIB.gf_cascade_fast(W1.handle, W2.handle, 1 if wrap else 0, q.pd, float(dcell), q.pR, q.pt, q.pc,
-                             64 if (precision or _precision) == "fp64" else 32, q.pout)
+    bits = 64 if (precision or _precision) == "fp64" else 32
+    srv = _servers.get((W1.handle, W2.handle, bool(wrap), bits)) if _servers else None
+    if srv is not None and srv.matches(dcell, arg[15: 15 + d], arg[12: 12 + d]):
+        rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
+    else:
+        rc = LIB.gf_cascade_fast(W1.handle, W2.handle, 1 if wrap else 0, q.pd, float(dcell), q.pR, q.pt, q.pc, bits,
+                                 q.pout)
     if rc:
         check(rc)
     n = 14 if d == 3 else 8
     return q.out[:n].copy().view(np.complex128)
+
+
+# ---------------------------------------------------------------------------
+# persistent haptic server (no kernel launch per query)
+
+_servers = {}
+
+
+class HapticServer:
+    """A resident query grid for one window pair (gf_server_*).
+
+    While it runs, `cascade` calls with the same windows, wrap flag,
+    precision and grid constants are answered through its mailbox instead of
+    a kernel launch per query.  Use as a context manager (stops on exit); the
+    device side also exits on its own after `idle_timeout_s` without queries.
+    """
+
+    def __init__(self, C1, C2, wrap, domega, dcell, center, precision=None, idle_timeout_s=30.0):
+        self.W1, self.W2 = as_device_window(C1), as_device_window(C2)
+        d = self.W1.ndim
+        self.bits = 64 if (precision or _precision) == "fp64" else 32
+        self.wrap = bool(wrap)
+        self.dcell = float(dcell)
+        self.dom = np.ascontiguousarray(domega, dtype=np.float64)[:d].copy()
+        self.center = np.ascontiguousarray(center, dtype=np.float64)[:d].copy()
+        sid = ctypes.c_uint64(0)
+        check(LIB.gf_server_start(self.W1.handle, self.W2.handle, int(self.wrap), dptr(self.dom), self.dcell,
+                                  dptr(self.center), self.bits, float(idle_timeout_s), ctypes.byref(sid)))
+        self.id = sid.value
+        self.key = (self.W1.handle, self.W2.handle, self.wrap, self.bits)
+        _servers[self.key] = self
+
+    def matches(self, dcell, dom, center):
+        return dcell == self.dcell and np.array_equal(dom, self.dom) and np.array_equal(center, self.center)
+
+    def stop(self):
+        if self.id:
+            if _servers.get(self.key) is self:
+                del _servers[self.key]
+            check(LIB.gf_server_stop(self.id))
+            self.id = 0
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.stop()
+
+    def __del__(self):
+        try:
+            self.stop()
+        except Exception:
+            pass
 
 
 def pack_poses(R, t_eff):

@@ -10,17 +10,44 @@
 
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 namespace gf {
 
 static thread_local std::string tl_error;
 void set_error(const std::string& msg) { tl_error = msg; }
 const char* last_error() { return tl_error.c_str(); }
+
+static std::mutex g_free_mu;
+static int g_servers_running = 0;
+static std::vector<void*> g_deferred;
+
+void device_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_free_mu);
+  if (g_servers_running > 0) g_deferred.push_back(p);
+  else cudaFree(p);
+}
+
+static void server_started() {
+  std::lock_guard<std::mutex> lk(g_free_mu);
+  ++g_servers_running;
+}
+
+static void server_stopped() {
+  std::lock_guard<std::mutex> lk(g_free_mu);
+  if (--g_servers_running == 0) {
+    for (void* p : g_deferred) cudaFree(p);
+    g_deferred.clear();
+  }
+}
 
 // ---------------------------------------------------------------------------
 // windows
@@ -34,10 +61,10 @@ struct Window {
   void* raw32 = nullptr;            // complex64 (lazy)
   void* packed[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [prec32?0:1][wrap]
   ~Window() {
-    cudaFree(raw64);
-    cudaFree(raw32);
+    device_free(raw64);
+    device_free(raw32);
     for (auto& p : packed)
-      for (auto q : p) cudaFree(q);
+      for (auto q : p) device_free(q);
   }
 };
 
@@ -92,13 +119,13 @@ static int ensure_context() {
 
 static int ensure_scratch(Context& c, int64_t n_partials, int64_t n_counters, cudaStream_t st) {
   if (n_partials > c.partials_cap) {
-    cudaFree(c.partials);
+    device_free(c.partials);
     c.partials = nullptr;
     GF_CUDA(cudaMalloc((void**)&c.partials, n_partials * sizeof(double)));
     c.partials_cap = n_partials;
   }
   if (n_counters > c.counters_cap) {
-    cudaFree(c.counters);
+    device_free(c.counters);
     c.counters = nullptr;
     GF_CUDA(cudaMalloc((void**)&c.counters, n_counters * sizeof(unsigned)));
     GF_CUDA(cudaMemsetAsync(c.counters, 0, n_counters * sizeof(unsigned), st));
@@ -426,6 +453,161 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
     GF_CUDA(launch_cascade(a, 1, st));
   }
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// persistent haptic server
+
+namespace {
+struct Mailbox {               // host-mapped, one per server
+  volatile unsigned long long seq;
+  volatile unsigned stop;
+  unsigned pad;
+  double pose[12];
+  double out[16];
+  volatile unsigned long long done;
+};
+struct Server {
+  int device = 0;
+  int d = 3;
+  cudaStream_t stream = nullptr;
+  Mailbox* mb = nullptr;       // host view
+  Mailbox* mb_dev = nullptr;   // device alias
+  void* dev_words = nullptr;   // dev_seq (8 B) + dev_pose (96 B)
+  double* partials = nullptr;
+  unsigned* counters = nullptr;
+  unsigned long long seq = 0;
+  bool running = false;
+};
+std::mutex g_srv_mu;
+std::unordered_map<uint64_t, std::unique_ptr<Server>> g_servers;
+uint64_t g_next_server = 1;
+
+Server* find_server(uint64_t id) {
+  std::lock_guard<std::mutex> lk(g_srv_mu);
+  auto it = g_servers.find(id);
+  return it == g_servers.end() ? nullptr : it->second.get();
+}
+
+int stop_server(Server* s) {
+  if (!s->running) return 0;
+  s->mb->stop = 1u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  s->mb->seq = ++s->seq;
+  GF_CUDA(cudaStreamSynchronize(s->stream));
+  s->running = false;
+  server_stopped();
+  return 0;
+}
+}  // namespace
+
+int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, double dcell, const double* center,
+                    int precision, double idle_timeout_s, uint64_t* server_id) {
+  GF_CHECK(domega && center && server_id, GF_EINVAL, "null argument");
+  int rc = ensure_context();
+  if (rc) return rc;
+  Window* w1 = find_window(h1);
+  Window* w2 = find_window(h2);
+  GF_CHECK(w1 && w2, GF_EINVAL, "unknown window handle");
+  auto s = std::make_unique<Server>();
+  GF_CUDA(cudaGetDevice(&s->device));
+  int lo = 0, hi = 0;
+  GF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  GF_CUDA(cudaStreamCreateWithPriority(&s->stream, cudaStreamNonBlocking, hi));
+  CascadeArgs a;
+  rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, s->stream);
+  if (rc) return rc;
+  GF_CHECK(a.variant == 1, GF_EINVAL, "the haptic server needs the default (direct) cascade variant");
+  plan_cascade(a, 1, 2 * 148);
+  GF_CHECK(a.single == 1, GF_EINTERNAL, "single-pose plan expected");
+  GF_CUDA(cudaHostAlloc((void**)&s->mb, sizeof(Mailbox), cudaHostAllocMapped));
+  std::memset((void*)s->mb, 0, sizeof(Mailbox));
+  GF_CUDA(cudaHostGetDevicePointer((void**)&s->mb_dev, (void*)s->mb, 0));
+  GF_CUDA(cudaMalloc(&s->dev_words, 8 + 12 * sizeof(double)));
+  GF_CUDA(cudaMemsetAsync(s->dev_words, 0, 8 + 12 * sizeof(double), s->stream));
+  GF_CUDA(cudaMalloc((void**)&s->partials, (size_t)a.blocks_per_pose * kNumMoments * sizeof(double)));
+  GF_CUDA(cudaMalloc((void**)&s->counters, sizeof(unsigned)));
+  GF_CUDA(cudaMemsetAsync(s->counters, 0, sizeof(unsigned), s->stream));
+  a.partials = s->partials;
+  a.counters = s->counters;
+  a.out = s->mb_dev->out;
+  a.done_flag = &s->mb_dev->done;
+  a.debug = nullptr;
+  ServerCtl ctl;
+  ctl.host_seq = &s->mb_dev->seq;
+  ctl.host_stop = &s->mb_dev->stop;
+  ctl.host_pose = s->mb_dev->pose;
+  ctl.dev_seq = (volatile unsigned long long*)s->dev_words;
+  ctl.dev_pose = (double*)((char*)s->dev_words + 8);
+  ctl.start_seq = 0;
+  ctl.idle_timeout_ns = (unsigned long long)((idle_timeout_s > 0 ? idle_timeout_s : 30.0) * 1e9);
+  auto tl0 = std::chrono::steady_clock::now();
+  server_started();
+  cudaError_t le = launch_cascade_server(a, ctl, s->stream);
+  if (le != cudaSuccess) server_stopped();
+  GF_CUDA(le);
+  if (getenv("GF_DEBUG_SERVER"))
+    fprintf(stderr, "[gf] server launch took %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count());
+  s->d = w1->d;
+  s->running = true;
+  std::lock_guard<std::mutex> lk(g_srv_mu);
+  *server_id = g_next_server++;
+  g_servers[*server_id] = std::move(s);
+  return 0;
+}
+
+int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, double* out) {
+  Server* s = find_server(server_id);
+  GF_CHECK(s && R && t_eff && out, GF_EINVAL, "unknown server or null argument");
+  GF_CHECK(s->running, GF_EINVAL, "server is not running (stopped or idle-timed out)");
+  embed_pose(s->d, R, t_eff, s->mb->pose);
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  const unsigned long long seq = ++s->seq;
+  s->mb->seq = seq;
+  auto t0 = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  while (s->mb->done != seq) {
+    if ((++spins & 0xffff) == 0) {
+      cudaError_t e = cudaStreamQuery(s->stream);
+      if (e != cudaErrorNotReady) {  // kernel exited (idle timeout) or failed
+        s->running = false;
+        server_stopped();
+        if (e != cudaSuccess) GF_CUDA(e);
+        GF_CHECK(s->mb->done == seq, GF_EINVAL, "server exited (idle timeout); start a new one");
+        break;
+      }
+      GF_CHECK(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(5), GF_EINTERNAL,
+               "haptic server did not answer within 5 s");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  if (s->d == 3) {
+    std::memcpy(out, s->mb->out, 14 * sizeof(double));
+  } else {
+    std::memcpy(out, s->mb->out, 6 * sizeof(double));
+    out[6] = s->mb->out[12];
+    out[7] = s->mb->out[13];
+  }
+  return 0;
+}
+
+int gf_server_stop(uint64_t server_id) {
+  std::unique_ptr<Server> s;
+  {
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    auto it = g_servers.find(server_id);
+    GF_CHECK(it != g_servers.end(), GF_EINVAL, "unknown server");
+    s = std::move(it->second);
+    g_servers.erase(it);
+  }
+  int rc = stop_server(s.get());
+  device_free(s->dev_words);
+  device_free(s->partials);
+  device_free(s->counters);
+  cudaFreeHost((void*)s->mb);
+  cudaStreamDestroy(s->stream);
+  return rc;
 }
 
 }  // extern "C"

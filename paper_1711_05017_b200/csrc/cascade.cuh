@@ -67,6 +67,18 @@ template <typename T> struct Acc26 {
   }
 };
 
+// Persistent haptic server mailbox plumbing (cascade_single.cu)
+struct ServerCtl {
+  volatile unsigned long long* host_seq;   // host-mapped: request sequence number
+  volatile unsigned* host_stop;            // host-mapped: stop request
+  const volatile double* host_pose;        // host-mapped: R (9) + t_eff (3)
+  volatile unsigned long long* dev_seq;    // device: forwarded sequence number
+  double* dev_pose;                        // device: forwarded pose
+  unsigned long long start_seq;
+  unsigned long long idle_timeout_ns;
+};
+cudaError_t launch_cascade_server(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st);
+
 int tiled_tile_count(const CascadeArgs& a, int ts);
 size_t tiled_smem_bytes(int precision, int ts, const int w[3]);
 int single_blocks(const CascadeArgs& a, int sms);

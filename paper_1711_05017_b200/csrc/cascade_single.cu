@@ -76,16 +76,16 @@ __device__ __forceinline__ double finalize_slot(const CascadeArgs& a, const Sing
   return dc * acc;
 }
 
+// One pose over all retained modes, spread across the grid; shared state is
+// passed in so the same body runs in the one-shot kernel and in the
+// persistent haptic server.  Non-final blocks return early (block-uniform).
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_single_kernel(CascadeArgs a) {
+__device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const double* src, SinglePose& sp, double* red,
+                                                 unsigned& ticket, unsigned char* smem_raw) {
   using P4 = typename pair4<T>::type;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   // dynamic: transpose buffer tr[26][257] (reduction) | px | py | pz
   T(*tr)[kThreads + 1] = reinterpret_cast<T(*)[kThreads + 1]>(smem_raw);
   cx<T>* ptab = reinterpret_cast<cx<T>*>(smem_raw + sizeof(T) * kNumMoments * (kThreads + 1) + 16);
-  __shared__ SinglePose sp;
-  __shared__ double red[kNumMoments];
-  __shared__ unsigned ticket;
 
   const int tid = threadIdx.x;
   unsigned long long* dbg = a.debug ? a.debug + (int64_t)blockIdx.x * 8 : nullptr;
@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   GF_STAMP(0)
   const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
-  const double* src = a.poses ? a.poses + a.pose_offset * 12 : a.pose_inline;
   if (tid < 9) {
     sp.R[tid] = src[tid];
     int ia = tid / 3, ib = tid % 3;
@@ -357,6 +356,73 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
 }
 
 template <typename T, bool WRAP>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_single_kernel(CascadeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SinglePose sp;
+  __shared__ double red[kNumMoments];
+  __shared__ unsigned ticket;
+  const double* src = a.poses ? a.poses + a.pose_offset * 12 : a.pose_inline;
+  single_pose_body<T, WRAP>(a, src, sp, red, ticket, smem_raw);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent haptic server: the grid stays resident (cooperative launch) and
+// serves one query per mailbox sequence number.  Block 0 polls the host-
+// mapped mailbox and forwards the pose to device memory; the other blocks
+// poll a device word.  No kernel launch per query.
+constexpr unsigned long long kServerStop = ~0ull;
+
+template <typename T, bool WRAP>
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_server_kernel(CascadeArgs a,
+                                                                                               ServerCtl ctl) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SinglePose sp;
+  __shared__ double red[kNumMoments];
+  __shared__ unsigned ticket;
+  __shared__ unsigned long long cur;
+  __shared__ double pose_s[12];
+  unsigned long long last = ctl.start_seq;
+  while (true) {
+    if (threadIdx.x == 0) {
+      unsigned long long sq;
+      if (blockIdx.x == 0) {
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while ((sq = *ctl.host_seq) == last) {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > ctl.idle_timeout_ns) {
+            sq = kServerStop;
+            break;
+          }
+        }
+        if (sq != kServerStop) {
+          __threadfence_system();
+          if (*ctl.host_stop) sq = kServerStop;
+          else
+            for (int k = 0; k < 12; ++k) ctl.dev_pose[k] = ctl.host_pose[k];
+        }
+        __threadfence();
+        *ctl.dev_seq = sq;
+      } else {
+        while ((sq = *ctl.dev_seq) == last) __nanosleep(32);
+        __threadfence();
+      }
+      cur = sq;
+    }
+    __syncthreads();
+    const unsigned long long sq = cur;
+    if (sq == kServerStop) break;
+    if (threadIdx.x < 12) pose_s[threadIdx.x] = __ldcg(ctl.dev_pose + threadIdx.x);  // bypass stale L1
+    __syncthreads();
+    CascadeArgs q = a;
+    q.done_seq = sq;
+    single_pose_body<T, WRAP>(q, pose_s, sp, red, ticket, smem_raw);
+    last = sq;
+    __syncthreads();
+  }
+}
+
+template <typename T, bool WRAP>
 cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
   size_t smem = sizeof(T) * kNumMoments * (kThreads + 1) + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
   static size_t configured = 0;
@@ -400,6 +466,34 @@ int single_blocks(const CascadeArgs& a, int sms) {
   if (const char* env = getenv("GF_SINGLE_CLUSTER")) g_cluster = atoi(env);  // experiments only
   b = (b / g_cluster) * g_cluster;  // whole clusters
   return (int)(b < g_cluster ? g_cluster : b);
+}
+
+template <typename T, bool WRAP>
+cudaError_t launch_server_t(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st) {
+  size_t smem = sizeof(T) * kNumMoments * (kThreads + 1) + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(cascade3d_server_kernel<T, WRAP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cascade3d_server_kernel<T, WRAP>, kThreads,
+                                                                smem);
+  if (e != cudaSuccess) return e;
+  if ((int64_t)per_sm * sms < a.blocks_per_pose) return cudaErrorCooperativeLaunchTooLarge;
+  CascadeArgs aa = a;
+  ServerCtl cc = ctl;
+  void* args[] = {&aa, &cc};
+  return cudaLaunchCooperativeKernel((const void*)cascade3d_server_kernel<T, WRAP>, dim3(a.blocks_per_pose),
+                                     dim3(kThreads), args, smem, st);
+}
+
+cudaError_t launch_cascade_server(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st) {
+  if (a.precision == 32)
+    return a.wrap ? launch_server_t<float, true>(a, ctl, st) : launch_server_t<float, false>(a, ctl, st);
+  return a.wrap ? launch_server_t<double, true>(a, ctl, st) : launch_server_t<double, false>(a, ctl, st);
 }
 
 cudaError_t launch_cascade_single(const CascadeArgs& a, cudaStream_t st) {

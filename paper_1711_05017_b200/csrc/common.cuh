@@ -22,6 +22,11 @@ enum GfStatus : int {
 void set_error(const std::string& msg);
 const char* last_error();
 
+// cudaFree synchronises the whole device; while a persistent haptic server
+// grid is resident that would wait for its idle timeout.  All engine frees go
+// through device_free, which defers them until no server is running.
+void device_free(void* p);
+
 #define GF_CUDA(expr)                                                            \
   do {                                                                           \
     cudaError_t _e = (expr);                                                     \

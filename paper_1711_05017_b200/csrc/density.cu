@@ -442,7 +442,7 @@ double __longlong_as_double_host(unsigned long long b) {
 
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() { cudaFree(p); }
+  ~DevBuf() { gf::device_free(p); }
 };
 
 int upload(const void* host, size_t bytes, DevBuf& b, cudaStream_t st) {

@@ -106,3 +106,19 @@ def test_cascade_batch_matches_single(be):
             want = oracle.cascade(C1, C2, False, (0.1,) * 3, 0.5, Rs[i], ts[i], np.array([0.1, 0.2, 0.3]))
             l1 = oracle.cascade_term_scales(C1, C2, False, (0.1,) * 3, 0.5, Rs[i], ts[i], np.array([0.1, 0.2, 0.3]))
             assert np.all(parity_tol(got[i], want, l1, 1e-4 if prec == "fp32" else 1e-10))
+
+
+def test_haptic_server_matches_one_shot(be):
+    rng = np.random.default_rng(21)
+    for w, wrap in ((32, False), (16, True)):
+        C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+        W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+        dom, c = (0.11, 0.11, 0.11), np.array([0.1, 0.2, -0.3])
+        poses = [(random_rotation(rng), rng.uniform(-1, 1, 3)) for _ in range(20)]
+        want = [be.cascade(W1, W2, wrap, dom, 0.4, R, t, c) for R, t in poses]
+        with be.HapticServer(W1, W2, wrap, dom, 0.4, c) as srv:
+            assert srv.key in be._servers
+            got = [be.cascade(W1, W2, wrap, dom, 0.4, R, t, c) for R, t in poses]
+        assert srv.key not in be._servers
+        for g, w_ in zip(got, want):
+            np.testing.assert_array_equal(g, w_)  # same kernel body, same reduction order
