@@ -383,9 +383,12 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   __shared__ double pose_s[12];
   unsigned long long last = ctl.start_seq;
   while (true) {
-    if (threadIdx.x == 0) {
-      unsigned long long sq;
-      if (blockIdx.x == 0) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      // warp 0 of block 0: lane 0 polls the host mailbox; then the pose and
+      // stop word are fetched by 13 lanes in parallel (one PCIe round trip)
+      const int lane = threadIdx.x;
+      unsigned long long sq = 0;
+      if (lane == 0) {
         unsigned long long t0, t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         while ((sq = *ctl.host_seq) == last) {
@@ -395,18 +398,26 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
             break;
           }
         }
-        if (sq != kServerStop) {
-          __threadfence_system();
-          if (*ctl.host_stop) sq = kServerStop;
-          else
-            for (int k = 0; k < 12; ++k) ctl.dev_pose[k] = ctl.host_pose[k];
-        }
-        __threadfence();
-        *ctl.dev_seq = sq;
-      } else {
-        while ((sq = *ctl.dev_seq) == last) __nanosleep(32);
-        __threadfence();
+        __threadfence_system();
       }
+      sq = __shfl_sync(0xffffffffu, sq, 0);
+      unsigned stop = 0;
+      if (sq != kServerStop) {
+        if (lane < 12) ctl.dev_pose[lane] = ctl.host_pose[lane];
+        if (lane == 12) stop = *ctl.host_stop;
+      }
+      stop = __shfl_sync(0xffffffffu, stop, 12);
+      if (stop) sq = kServerStop;
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        *ctl.dev_seq = sq;
+        cur = sq;
+      }
+    } else if (blockIdx.x != 0 && threadIdx.x == 0) {
+      unsigned long long sq;
+      while ((sq = *ctl.dev_seq) == last) __nanosleep(32);
+      __threadfence();
       cur = sq;
     }
     __syncthreads();
