@@ -484,6 +484,19 @@ def measure_stages(args, rank, world, fp32_peak):
                      "frac": achieved / fp32_peak, "work": f"240 flop x live modes ({live:.3f} of m')"},
         "projected_1e6_poses_s": 1e6 / (len(ts) / (ms * 1e-3)),
     }
+    if rank == 0 and not args.no_cpu:
+        core = reference_core()
+        C1h, C2h = a1._win.__array__(), a2._win.__array__()
+        n_cpu = 0
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < args.stage_cpu_seconds and n_cpu < len(ts):
+            core.cascade_3d(C1h, C2h, False, *g3.delta_omega(), dcell, np.ascontiguousarray(Rs[n_cpu]),
+                            np.ascontiguousarray(t_eff[n_cpu]), c)
+            n_cpu += 1
+        dt = time.perf_counter() - t0
+        out["sweep_C3"]["cpu_baseline"] = {
+            "value": n_cpu / dt, "unit": "poses/s", "cores": 1, "kind": "reference",
+            "sample": f"{n_cpu} of the same poses through _core.cascade_3d (oracle/_ref), 1 thread"}
     del a1, a2, poses, res
     torch.cuda.empty_cache()
 
@@ -503,6 +516,18 @@ def measure_stages(args, rank, world, fp32_peak):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "scaling_plan": "slab-decomposed across ranks with one all-to-all (parallel.score_field_slab)",
     }
+    if rank == 0 and not args.no_cpu:
+        nc = 128
+        rngc = np.random.default_rng(SEED)
+        Cc1 = rngc.normal(size=(nc,) * 3) + 1j * rngc.normal(size=(nc,) * 3)
+        Cc2 = rngc.normal(size=(nc,) * 3) + 1j * rngc.normal(size=(nc,) * 3)
+        t0 = time.perf_counter()
+        oracle.score_field(Cc1, Cc2, True, (nc,) * 3, (-1.0,) * 3, 2.0 / nc, R4[0])
+        dt = time.perf_counter() - t0
+        out["field_C4"]["cpu_baseline"] = {
+            "value": nc ** 3 / dt, "unit": "voxels/s", "cores": 1, "kind": "port",
+            "sample": f"oracle.score_field (numpy restatement of energy.score_field, energy.py:309-344) at "
+                      f"{nc}^3 full spectrum, one rotation, {dt:.1f} s (512^3 does not fit a bounded CPU sample)"}
     del b1, b2
     torch.cuda.empty_cache()
 
@@ -514,6 +539,15 @@ def measure_stages(args, rank, world, fp32_peak):
     out["window_W"] = {"workload": "forward DFT + truncation + centring, 256^3 complex128 field -> 96^3 window",
                        "ms": ms, "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm,
                                               "unit": "GB/s", "frac": alg / (ms * 1e-3) / 1e9 / hbm}}
+    if rank == 0 and not args.no_cpu:
+        fh = fw.values.reshape((256,) * 3)
+        t0 = time.perf_counter()
+        A = oracle.forward_dft(fh, (256,) * 3, (-1.0,) * 3, 2.0 / 256)
+        oracle.center_window(A, (256,) * 3, (-1.0,) * 3, 2.0 / 256, 96)
+        dt = time.perf_counter() - t0
+        out["window_W"]["cpu_baseline"] = {"value": dt * 1e3, "unit": "ms", "cores": 1, "kind": "port",
+                                           "sample": "oracle.forward_dft + center_window (numpy pocketfft, as "
+                                                     "spectral.py:114-195) on the same 256^3 field"}
     del fw
     torch.cuda.empty_cache()
 
@@ -529,6 +563,26 @@ def measure_stages(args, rank, world, fp32_peak):
     out["density_D"] = {"workload": f"affinity_field, bored block ({nf} faces) on 64^3, float64 bit-exact flags",
                         "voxels_per_s": gd.node_count / dt, "node_face_pairs_per_s": gd.node_count * nf / dt,
                         "ms": dt * 1e3, "excluded": fd.stats["excluded"], "unresolved": fd.stats["unresolved_nodes"]}
+    if rank == 0 and not args.no_cpu:
+        core = reference_core()
+        gc = sc.grid(16)
+        P = gc.points()
+        m = sc.fixed.mesh
+        tri = np.ascontiguousarray(m.triangles)
+        t0 = time.perf_counter()
+        xi = np.empty(len(P))
+        core.distance_3d(*sc.fixed.bvh(), tri, P, xi, 0, len(P))
+        wind = np.empty(len(P))
+        core.winding_3d(tri, P, wind, 0, len(P))
+        iplus = np.empty(len(P), dtype=np.complex128)
+        res = np.zeros(len(P))
+        cl = np.zeros(len(P), dtype=np.int64)
+        core.sweep_3d(tri, m.normals, m.areas, P, np.maximum(xi, 0.25 * gc.spacing), 0.5, 1 / (4 * np.pi), 0.02, 16,
+                      0.25 * gc.spacing, iplus, res, cl, 0, len(P))
+        dt = time.perf_counter() - t0
+        out["density_D"]["cpu_baseline"] = {
+            "value": gc.node_count * nf / dt, "unit": "node-face pairs/s", "cores": 1, "kind": "reference",
+            "sample": f"_core distance_3d + winding_3d + sweep_3d (oracle/_ref) for the same part on 16^3, {dt:.1f} s"}
     return out
 
 
@@ -545,6 +599,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--sweep-poses", type=int, default=16384)
+    ap.add_argument("--stage-cpu-seconds", type=float, default=4.0)
     ap.add_argument("--field-n", type=int, default=512)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
