@@ -206,6 +206,8 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
     a.center[ax] = (ax < w1->d) ? center[ax] : 0.0;
   }
   for (int ax = 0; ax < w1->d; ++ax) GF_CHECK(a.dom[ax] > 0.0, GF_EINVAL, "domega must be positive");
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) a.rdom[i][j] = a.dom[i] / a.dom[j];
   a.dcell = dcell;
   a.seg_len = g_run_length;
   a.variant = g_variant;

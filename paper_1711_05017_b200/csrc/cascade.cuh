@@ -15,6 +15,7 @@ struct CascadeArgs {
   int wrap;
   int precision;         // 32 or 64
   double dom[3];         // frequency spacing per axis
+  double rdom[3][3];     // dom[i] / dom[j] (host-computed)
   double dcell;          // 1 / (N^d dV)
   double center[3];      // grid centre c
   // poses: `poses` (device, n x 12 doubles: R row-major then t_eff) or,

@@ -101,7 +101,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   if (tid < 9) {
     sp.R[tid] = src[tid];
     int ia = tid / 3, ib = tid % 3;
-    sp.mu[ia][ib] = -src[ib * 3 + ia] * (a.dom[ib] / a.dom[ia]);
+    sp.mu[ia][ib] = -src[ib * 3 + ia] * a.rdom[ib][ia];
   }
   if (tid >= 16 && tid < 19) sp.targ[tid - 16] = a.dom[tid - 16] * src[9 + tid - 16];
   if (tid >= 32 && tid < 32 + 27) {  // A_g = Omega_g R (_core.pyx:615-626)
@@ -111,7 +111,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     if (g == 0) Aab = ax == 0 ? 0.0 : (ax == 1 ? -Rr[6 + bb] : Rr[3 + bb]);
     else if (g == 1) Aab = ax == 0 ? Rr[6 + bb] : (ax == 1 ? 0.0 : -Rr[bb]);
     else Aab = ax == 0 ? -Rr[3 + bb] : (ax == 1 ? Rr[bb] : 0.0);
-    sp.cg[g][bb][ax] = -Aab * (a.dom[ax] / a.dom[bb]);
+    sp.cg[g][bb][ax] = -Aab * a.rdom[ax][bb];
   }
   if (tid >= 64 && tid < 64 + 9) {  // q_g = A_g c
     const int g = (tid - 64) / 3, ax = (tid - 64) % 3;
@@ -130,7 +130,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   if (tid >= 128 && tid < 140) {
     const int ia = (tid - 128) / 4, ib = (tid - 128) % 4;
     sp.ufix[ia][ib] = ib == 3 ? to_fix32((double)(ia == 0 ? hx : (ia == 1 ? hy : hz)))
-                              : to_fix32(-src[ib * 3 + ia] * (a.dom[ib] / a.dom[ia]));
+                              : to_fix32(-src[ib * 3 + ia] * a.rdom[ib][ia]);
   }
   __syncthreads();
   if (tid == 0) {
