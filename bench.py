@@ -442,6 +442,9 @@ class _Asset:
     def window(self, m_prime=None):
         return self._win, self._wrap
 
+    def max_modes(self):
+        return int(np.prod(self._win.shape))
+
 
 def measure_stages(args, rank, world, fp32_peak):
     import torch
@@ -531,6 +534,26 @@ def measure_stages(args, rank, world, fp32_peak):
     del b1, b2
     torch.cuda.empty_cache()
 
+    # --- C5: bolt-nut 256^3, K=64 (w=128), screw trajectory paced at 1 kHz
+    from paper_1711_05017_b200.haptic import HapticSession
+
+    n5, w5, dom5 = 256, 128, 4.37
+    g5 = SampleGrid(3, (n5,) * 3, (-0.5 * dom5,) * 3, dom5 / n5)
+    f5 = _Asset(g5, backend.DeviceWindow(mk(w5)), False), _Asset(g5, backend.DeviceWindow(mk(w5)), False)
+    frames = args.haptic_frames
+    th = np.linspace(0.0, 4.0 * np.pi, frames)  # two turns
+    pitch = 0.1
+    R5 = np.stack([axis_rot(2, a) for a in th])
+    t5 = np.stack([np.array([0.0, 0.0, 0.3 - pitch * a / (2 * np.pi)]) for a in th])
+    sess = HapticSession(f5[0], f5[1], None)
+    sess.run(R5[:50], t5[:50], rate_hz=1000.0)  # warm
+    run = sess.run(R5, t5, rate_hz=1000.0)
+    out["haptic_C5"] = {"workload": f"bolt-nut 256^3 grid, K=64 (w=128, m'={w5 ** 3}), {frames}-frame screw "
+                                    "trajectory (2 turns, pitch 0.1) paced at 1 kHz, one evaluate per frame, fp32",
+                        **run, "budget_us": 1000.0}
+    del f5, sess
+    torch.cuda.empty_cache()
+
     # --- W: forward centred window 256^3 -> w = 96 (complex128 field -> complex128 window)
     gw = SampleGrid(3, (256,) * 3, (-1.0,) * 3, 2.0 / 256)
     fw = ComplexField(gw, torch.randn(256 ** 3, dtype=torch.complex128, device=dev, generator=gen))
@@ -600,6 +623,7 @@ def main():
     ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--sweep-poses", type=int, default=16384)
     ap.add_argument("--stage-cpu-seconds", type=float, default=4.0)
+    ap.add_argument("--haptic-frames", type=int, default=1000)
     ap.add_argument("--field-n", type=int, default=512)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":

@@ -1,0 +1,101 @@
+"""Haptic session driver: the per-frame servo loop.
+
+Follows the reference's sandbox session (`Session.eval_current` /
+`Session.step_damped`, /root/reference/pkg/src/geofield/service.py:66-126),
+in 3D and on the GPU:
+
+* `eval_current` is one `evaluate` (one single-query kernel, or the resident
+  `backend.HapticServer` when one runs for the pair);
+* `step_damped` takes a first-order step dx = (F / c) dt clamped to half a
+  cell and, if the energy rises, halves it up to three more times.  The
+  reference evaluates those trials one after another (up to 4 extra
+  evaluate calls per frame); here all four trial poses go to ONE batched
+  cascade launch and the first trial (in the reference's order) whose energy
+  does not exceed the current one is taken -- the same decision, one launch.
+* `run` paces a trajectory at a fixed servo rate (the paper's 1 kHz loop,
+  PAPER.md:317-321) and records per-frame latency and deadline misses.
+"""
+
+from __future__ import annotations
+
+import statistics
+import time
+
+import numpy as np
+
+from . import backend
+from .energy import Configuration, EnergyEval, evaluate
+
+__all__ = ["HapticSession"]
+
+
+class HapticSession:
+    def __init__(self, fixed, moving, m_prime=None, damping=1.0, frame_dt=1e-3, rotation=None, translation=None):
+        self.fixed, self.moving, self.modes = fixed, moving, m_prime
+        g = fixed.grid
+        self.spacing = g.spacing
+        self.damping = float(damping)
+        self.frame_dt = float(frame_dt)
+        d = g.dimension
+        self.rotation = np.eye(d) if rotation is None else np.asarray(rotation, dtype=np.float64)
+        self.translation = np.zeros(d) if translation is None else np.asarray(translation, dtype=np.float64)
+        self.stats = []
+
+    def config(self):
+        return Configuration(self.rotation, self.translation)
+
+    def eval_current(self):
+        ev = evaluate(self.fixed, self.moving, self.config(), m_prime=self.modes)
+        self.stats.append(ev.eval_time_us)
+        return ev
+
+    def _trial_energies(self, trials):
+        """Energies of several translations at the current rotation, one launch."""
+        import torch
+
+        g = self.fixed.grid
+        c = g.center()
+        C1, wrap1 = self.fixed.window(self.modes)
+        C2, wrap2 = self.moving.window(self.modes)
+        R = np.broadcast_to(self.rotation, (len(trials),) + self.rotation.shape)
+        t_eff = np.asarray(trials) - c + self.rotation @ c
+        poses = torch.from_numpy(backend.pack_poses(R, t_eff)).cuda()
+        dcell = 1.0 / (g.node_count * g.cell_volume)
+        out = backend.cascade_batch(C1, C2, wrap1 and wrap2, g.delta_omega(), dcell, c, poses).cpu().numpy()
+        return -out[:, 0]  # energy = -Re(score)
+
+    def step_damped(self, ev: EnergyEval):
+        """One damped descent step with backtracking (service.py:105-126)."""
+        step = (ev.force / self.damping) * self.frame_dt
+        norm = float(np.linalg.norm(step))
+        limit = 0.5 * self.spacing
+        if norm > limit:
+            step = step * (limit / norm)
+        trials = [self.translation + step * 0.5 ** k for k in range(4)]
+        energies = self._trial_energies(trials)
+        for trial, e in zip(trials, energies):
+            if e <= ev.energy:
+                self.translation = trial
+                return True
+        return False  # every trial climbed: hold the pose
+
+    def run(self, rotations, translations, rate_hz=1000.0):
+        """Pace a pose trajectory at `rate_hz`; returns latency stats and misses."""
+        period = 1.0 / rate_hz
+        lat, misses = [], 0
+        t_next = time.perf_counter()
+        for R, t in zip(rotations, translations):
+            self.rotation, self.translation = np.asarray(R), np.asarray(t)
+            t0 = time.perf_counter()
+            self.eval_current()
+            dt = time.perf_counter() - t0
+            lat.append(dt * 1e6)
+            if dt > period:
+                misses += 1
+            t_next += period
+            while time.perf_counter() < t_next:  # servo pacing (busy wait: haptic threads spin)
+                pass
+        lat.sort()
+        pct = lambda p: lat[min(len(lat) - 1, int(p * len(lat)))]  # noqa: E731  (cli.py:357-361)
+        return {"frames": len(lat), "p50_us": statistics.median(lat), "p95_us": pct(0.95), "p99_us": pct(0.99),
+                "max_us": lat[-1], "deadline_misses": misses, "rate_hz": rate_hz}
