@@ -29,6 +29,7 @@
 #include "fft_core.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 #include <map>
 #include <mutex>
@@ -146,6 +147,106 @@ __global__ void __launch_bounds__(B*(N >= 8 ? N / 8 : 1)) fft_kernel(FftArgs a) 
   }
 }
 
+// Strided axes, complex64: one thread owns the same FFT positions of two
+// adjacent lines (b, b + 1), so every global access is a 16-byte vector and
+// half as many load/store instructions feed the LSU (the ncu stall of the
+// 8-byte version was lg_throttle).  Same semantics as fft_kernel; requires an
+// even contiguous extent (the lines of a pair are both live or both dead).
+template <int N, int B>
+__global__ void __launch_bounds__(B / 2 * (N / 8), 2) fft_pair_kernel(FftArgs a) {
+  using T = float;
+  constexpr int TPL = N / 8;
+  constexpr int LD = LineLD<T, N>::value;
+  constexpr int BP = B / 2;
+  extern __shared__ __align__(16) unsigned char fft_smem[];
+  cx<T>* buf = reinterpret_cast<cx<T>*>(fft_smem);
+  const int tid = threadIdx.x;
+  const int ax = a.axis;
+  const int bp = tid % BP, j = tid / BP;
+  const int Lin = a.shape_in[ax], Lout = a.shape_out[ax];
+  const float4* __restrict__ in = reinterpret_cast<const float4*>(a.in);
+  float4* __restrict__ out = reinterpret_cast<float4*>(a.out);
+  const cx<T>* __restrict__ tw = reinterpret_cast<const cx<T>*>(a.tw);
+  const int s2 = a.shape_in[2];
+  const int ptiles = (s2 + B - 1) / B;
+  const int o = blockIdx.x / ptiles, p = (blockIdx.x % ptiles) * B + 2 * bp;
+  const bool live = p < s2;
+  int64_t base_in, base_out, st_in, st_out;  // in float4 (pair) units
+  if (ax == 0) {
+    base_in = ((int64_t)o * s2 + p) / 2;
+    base_out = ((int64_t)o * a.shape_out[2] + p) / 2;
+    st_in = (int64_t)a.shape_in[1] * s2 / 2;
+    st_out = (int64_t)a.shape_out[1] * a.shape_out[2] / 2;
+  } else {
+    base_in = ((int64_t)o * a.shape_in[1] * s2 + p) / 2;
+    base_out = ((int64_t)o * a.shape_out[1] * a.shape_out[2] + p) / 2;
+    st_in = s2 / 2;
+    st_out = a.shape_out[2] / 2;
+  }
+  cx<T> v0[8], v1[8];
+  const int hin = Lin / 2;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int pos = j + r * TPL;
+    int src, m;
+    if (a.in_centered) {
+      m = pos < N / 2 ? pos : pos - N;
+      src = m + hin;
+      if (src < 0 || src >= Lin) src = -1;
+    } else {
+      m = pos;
+      src = pos;
+    }
+    cx<T> x0 = mk<T>(0, 0), x1 = mk<T>(0, 0);
+    if (live && src >= 0) {
+      const float4 q = __ldcs(&in[base_in + (int64_t)src * st_in]);
+      x0 = mk<T>(q.x, q.y);
+      x1 = mk<T>(q.z, q.w);
+      if (a.in_phase_kind) {
+        const cx<T> ph = phase_factor<T>(a.in_phase_kind, a.in_phase, m);
+        x0 = x0 * ph;
+        x1 = x1 * ph;
+      }
+    }
+    v0[r] = x0;
+    v1[r] = x1;
+  }
+  cx<T>* line0 = buf + (2 * bp) * LD;
+  cx<T>* line1 = line0 + LD;
+  // park line 1 in its own (so far untouched) buffer while line 0 transforms
+#pragma unroll
+  for (int r = 0; r < 8; ++r) line1[sidx<T>(j + r * TPL)] = v1[r];
+  fft_line<T, N>(v0, line0, j, tw, a.sign);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v1[r] = line1[sidx<T>(j + r * TPL)];
+  fft_line<T, N>(v1, line1, j, tw, a.sign);
+  if (!live) return;
+  const int hout = Lout / 2;
+  const T sc = (T)a.scale;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int pos = j + r * TPL;
+    int dst, m;
+    if (a.out_centered) {
+      m = pos < N / 2 ? pos : pos - N;
+      dst = m + hout;
+      if (dst < 0 || dst >= Lout) continue;
+    } else {
+      m = pos;
+      dst = pos;
+    }
+    cx<T> y0 = line0[sidx<T>(pos)], y1 = line1[sidx<T>(pos)];
+    y0 = mk<T>(y0.re * sc, y0.im * sc);
+    y1 = mk<T>(y1.re * sc, y1.im * sc);
+    if (a.out_phase_kind) {
+      const cx<T> ph = phase_factor<T>(a.out_phase_kind, a.out_phase, m);
+      y0 = y0 * ph;
+      y1 = y1 * ph;
+    }
+    __stcs(&out[base_out + (int64_t)dst * st_out], make_float4(y0.re, y0.im, y1.re, y1.im));
+  }
+}
+
 template <typename T>
 __global__ void twiddle_kernel(cx<T>* tw, int n, int sign) {
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
@@ -201,6 +302,28 @@ cudaError_t launch_nb(const FftArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+bool pair_enabled() {
+  static const bool on = !getenv("GF_FFT_NOPAIR");
+  return on;
+}
+
+template <int N, int B>
+cudaError_t launch_pair(const FftArgs& a, cudaStream_t st) {
+  const int so = a.axis == 0 ? a.shape_in[1] : a.shape_in[0];
+  const int64_t blocks = (int64_t)so * ceil_div(a.shape_in[2], B);
+  constexpr size_t smem = sizeof(cx<float>) * B * LineLD<float, N>::value;
+  if (smem > 48 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(fft_pair_kernel<N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+  }
+  fft_pair_kernel<N, B><<<(unsigned)blocks, B / 2 * (N / 8), smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 // lines per CTA: strided axes need >= 128 contiguous bytes per row per CTA
 // (B = 16 complex64 / 8 complex128) for full-sector, full-line coalescing;
 // the contiguous axis only needs enough threads (B * N / 8 >= 256).
@@ -211,6 +334,9 @@ cudaError_t launch_n(const FftArgs& a, cudaStream_t st) {
   constexpr int B_thr = (256 / TPL) < 1 ? 1 : (256 / TPL) > 32 ? 32 : (256 / TPL);
   constexpr int B_str = (B_row > B_thr ? B_row : B_thr) * TPL > 1024 ? 1024 / TPL : (B_row > B_thr ? B_row : B_thr);
   if (a.axis == 2) return launch_nb<T, N, B_thr>(a, st);
+  if constexpr (sizeof(T) == 4 && N >= 64 && N <= 512) {
+    if (a.shape_in[2] % 2 == 0 && a.shape_out[2] % 2 == 0 && pair_enabled()) return launch_pair<N, 16>(a, st);
+  }
   return launch_nb<T, N, B_str>(a, st);
 }
 

@@ -65,6 +65,27 @@ template <typename T> __device__ __forceinline__ cx<T> phase_factor(int kind, do
 }
 
 
+// v[r] *= t^r, r = 1..R-1.  One table load per thread and stage (lanes read
+// consecutive entries) instead of R-1 strided ones, which made the twiddle
+// reads -- not the data -- the L1 bottleneck of contiguous-axis passes; the
+// powers by repeated squaring cost < 3 ulp at R = 8.
+template <typename T, int R> __device__ __forceinline__ void twiddle_powers(cx<T>* v, cx<T> t) {
+  if constexpr (R >= 2) v[1] = v[1] * t;
+  if constexpr (R >= 4) {
+    const cx<T> t2 = t * t;
+    const cx<T> t3 = t2 * t;
+    v[2] = v[2] * t2;
+    v[3] = v[3] * t3;
+    if constexpr (R >= 8) {
+      const cx<T> t4 = t2 * t2;
+      v[4] = v[4] * t4;
+      v[5] = v[5] * (t4 * t);
+      v[6] = v[6] * (t3 * t3);
+      v[7] = v[7] * (t4 * t3);
+    }
+  }
+}
+
 // Shared-memory line layout: one pad element every 128 bytes, so the
 // stride-8 stores of the first radix-8 stage (positions 8 j + r) spread over
 // the banks instead of piling onto two of them.
@@ -99,10 +120,7 @@ __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<
       for (int r = 0; r < 8; ++r) v[r] = line[sidx<T>(j + r * TPL)];
     }
     const int k = j & (Ns - 1);
-    if (Ns > 1) {
-#pragma unroll
-      for (int r = 1; r < 8; ++r) v[r] = v[r] * ldtw(&tw[(r * k * (N / (Ns * 8))) & (N - 1)]);
-    }
+    if (Ns > 1) twiddle_powers<T, 8>(v, ldtw(&tw[k * (N / (Ns * 8))]));
     dft8(v, sign);
     const int idx = (j - k) * 8 + k;
     __syncthreads();
@@ -126,10 +144,7 @@ __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<
 #pragma unroll
       for (int r = 0; r < R; ++r) u[r] = v[q + r * per];
       const int k = jj & (Ns - 1);
-      if (Ns > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) u[r] = u[r] * ldtw(&tw[(r * k * (N / (Ns * R))) & (N - 1)]);
-      }
+      if (Ns > 1) twiddle_powers<T, R>(u, ldtw(&tw[k * (N / (Ns * R))]));
       if constexpr (R == 4) dft4(u, sign);
       else dft2(u[0], u[1]);
 #pragma unroll

@@ -20,6 +20,7 @@
 #include "fft_core.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 extern "C" int gf_fft_pass(int precision, const void* in, void* out, const int32_t* shape_in,
                            const int32_t* shape_out, int axis, int n, int in_centered, int out_centered, int sign,
@@ -44,6 +45,9 @@ struct RotArgs {
   double tie_eps;
   int kx0, nkx;    // window x-planes [kx0, kx0 + nkx) (slab decomposition)
   void* out;       // (nkx, w1, w2) complex<T>
+  double mu[3][3];       // u_a = h_a + sum_b mu[a][b] kappa_b
+  long long ufix[3][3];  // to_fix32(mu)
+  int perm[3];           // brick lane order: fastest, middle, slowest mode axis
 };
 
 __device__ __forceinline__ double exact_u_f(const double* R, const double* dom, int a, int kx, int ky, int kz, int hx,
@@ -298,6 +302,122 @@ cudaError_t launch_zpass_w(const ZArgs& a, cudaStream_t st) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Brick-ordered product kernel: each CTA owns an 8 x 8 x 8 brick of window
+// modes (2 per thread), so the rotated footprint of a CTA in C2 is a compact
+// rotated brick -- each C2 sector comes from DRAM about once even when the
+// packed window (2.2 GB at 512^3) is far larger than L2.  The gather is
+// L1-wavefront bound, so lanes are laid out along the mode axes whose steps
+// move least across C2's 128-byte rows: the fastest lane axis (`perm[0]`) is
+// the mode axis with the largest component along C2's contiguous axis.  The
+// gathered V * phase goes through shared memory and the C1 read and Q write
+// are done in z-fastest order, coalesced.  fp32 indices in 32.32 fixed point.
+template <typename T, bool WRAP>
+__global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a, const cx<T>* __restrict__ ptx,
+                                                            const cx<T>* __restrict__ pty,
+                                                            const cx<T>* __restrict__ ptz) {
+  using P4 = typename pair4<T>::type;
+  __shared__ cx<T> sq[8 * 73];
+  const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
+  const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
+  const int nbz = (w2 + 7) / 8, nby = (w1 + 7) / 8;
+  const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
+  const int t = threadIdx.x;
+  const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
+  const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
+  const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
+  cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
+  const T eps = (T)a.tie_eps;
+  const int pf = a.perm[0], pm = a.perm[1];
+  // C1 for the epilogue's (z-fastest) modes, issued before the gathers
+  cx<T> c1v[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int oz = t & 7, oy = (t >> 3) & 7, ox = (t >> 6) + 4 * h;
+    const int kxl = bx * 8 + ox, ky = by * 8 + oy, kz = bz * 8 + oz;
+    c1v[h] = mk<T>(1, 0);
+    if (a.C1 && kxl < a.nkx && ky < w1 && kz < w2) c1v[h] = C1[((int64_t)(a.kx0 + kxl) * w1 + ky) * w2 + kz];
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o_f = t & 7, o_m = (t >> 3) & 7, o_s = (t >> 6) + 4 * h;
+    const int ox = pf == 0 ? o_f : (pm == 0 ? o_m : o_s);
+    const int oy = pf == 1 ? o_f : (pm == 1 ? o_m : o_s);
+    const int oz = pf == 2 ? o_f : (pm == 2 ? o_m : o_s);
+    const int kxl = bx * 8 + ox, ky = by * 8 + oy, kz = bz * 8 + oz;
+    if (kxl >= a.nkx || ky >= w1 || kz >= w2) continue;
+    const int kx = a.kx0 + kxl;
+    const int kk[3] = {kx - hx, ky - hy, kz - hz};
+    T fl[3], f[3];
+    if constexpr (sizeof(T) == 4) {
+      unsigned lo[3];
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const long long u = ((long long)(ax == 0 ? hx : (ax == 1 ? hy : hz)) << 32) +
+                            (long long)kk[0] * a.ufix[ax][0] + (long long)kk[1] * a.ufix[ax][1] +
+                            (long long)kk[2] * a.ufix[ax][2];
+        lo[ax] = fix_lo(u);
+        fl[ax] = (T)fix_floor(u);
+        f[ax] = fix_frac(lo[ax]);
+      }
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if ((ax < 2 || a.dim == 3) && fix_tie(lo[ax])) {
+          double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+          double fe = floor(ue);
+          fl[ax] = (T)fe;
+          f[ax] = (T)(ue - fe);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        double h0 = ax == 0 ? hx : (ax == 1 ? hy : hz);
+        double u = h0 + a.mu[ax][0] * kk[0] + a.mu[ax][1] * kk[1] + a.mu[ax][2] * kk[2];
+        fl[ax] = floor(u);
+        f[ax] = u - fl[ax];
+        if ((ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
+          double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, (int)h0);
+          double fe = floor(ue);
+          fl[ax] = fe;
+          f[ax] = ue - fe;
+        }
+      }
+    }
+    int ix = (int)fl[0], iy = (int)fl[1], iz = (int)fl[2];
+    cx<T> V = mk<T>(0, 0);
+    bool live = true;
+    if (WRAP) {
+      ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
+      iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
+      iz = iz < 0 ? iz + w2 : (iz >= w2 ? iz - w2 : iz);
+    } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
+               (unsigned)(iz + 1) > (unsigned)w2) {
+      live = false;
+    }
+    if (live) {
+      const P4* p = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
+      P4 e00 = ldg_pair(p), e10 = ldg_pair(p + sx), e01 = ldg_pair(p + sy), e11 = ldg_pair(p + sx + sy);
+      const T fu = f[0], fv = f[1], fs = f[2];
+      cx<T> a00 = lerp(mk<T>(e00.x, e00.y), mk<T>(e10.x, e10.y), fu);
+      cx<T> a01 = lerp(mk<T>(e00.z, e00.w), mk<T>(e10.z, e10.w), fu);
+      cx<T> a10 = lerp(mk<T>(e01.x, e01.y), mk<T>(e11.x, e11.y), fu);
+      cx<T> a11 = lerp(mk<T>(e01.z, e01.w), mk<T>(e11.z, e11.w), fu);
+      V = lerp(lerp(a00, a10, fv), lerp(a01, a11, fv), fs);
+    }
+    sq[ox * 73 + oy * 9 + oz] = V * ((ptx[kx] * pty[ky]) * ptz[kz]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int oz = t & 7, oy = (t >> 3) & 7, ox = (t >> 6) + 4 * h;
+    const int kxl = bx * 8 + ox, ky = by * 8 + oy, kz = bz * 8 + oz;
+    if (kxl >= a.nkx || ky >= w1 || kz >= w2) continue;
+    const cx<T> q = c1v[h] * sq[ox * 73 + oy * 9 + oz];
+    out[((int64_t)kxl * w1 + ky) * w2 + kz] = q;
+  }
+}
+
 }  // namespace
 }  // namespace gf
 
@@ -340,16 +460,51 @@ int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double* d
   double floor_eps = precision == 32 ? 1e-4 : 1e-9;
   a.tie_eps = eps > floor_eps ? eps : floor_eps;
   a.out = out_dev;
-  int64_t n = (int64_t)a.nkx * a.w[1] * a.w[2];
-  unsigned grid = (unsigned)(ceil_div(n, 256) < 148 * 16 ? ceil_div(n, 256) : 148 * 16);
+  for (int i = 0; i < 3; ++i)
+    for (int jj = 0; jj < 3; ++jj) {
+      a.mu[i][jj] = -a.R[jj * 3 + i] * (a.dom[jj] / a.dom[i]);
+      a.ufix[i][jj] = to_fix32(a.mu[i][jj]);
+    }
+  // lane order: fastest along the mode axis whose u-step is most aligned with
+  // C2's contiguous (z) axis, then the one most aligned with y
+  {
+    int pf = 0;
+    for (int b = 1; b < 3; ++b)
+      if (fabs(a.mu[2][b]) > fabs(a.mu[2][pf])) pf = b;
+    int c0 = (pf + 1) % 3, c1 = (pf + 2) % 3;
+    int pm = fabs(a.mu[1][c0]) >= fabs(a.mu[1][c1]) ? c0 : c1;
+    a.perm[0] = pf;
+    a.perm[1] = pm;
+    a.perm[2] = 3 - pf - pm;
+  }
+  // separable phase tables exp(2 pi i kappa_a dw_a s_a)
+  const size_t esz = precision == 32 ? 8 : 16;
+  void* tabs = nullptr;
+  GF_CUDA(cudaMallocAsync(&tabs, esz * (a.w[0] + a.w[1] + a.w[2]), st));
+  void* px = tabs;
+  void* py = (char*)tabs + esz * a.w[0];
+  void* pz = (char*)tabs + esz * (a.w[0] + a.w[1]);
+  const double t0 = a.dom[0] * a.s[0], t1 = a.dom[1] * a.s[1], t2 = a.dom[2] * a.s[2];
+  const unsigned bricks = (unsigned)(ceil_div(a.nkx, 8) * ceil_div(a.w[1], 8) * ceil_div(a.w[2], 8));
   if (precision == 32) {
-    if (wrap) rotate_product_kernel<float, true><<<grid, 256, 0, st>>>(a);
-    else rotate_product_kernel<float, false><<<grid, 256, 0, st>>>(a);
+    phase_tables_kernel<float><<<4, 256, 0, st>>>((cx<float>*)px, (cx<float>*)py, (cx<float>*)pz, a.w[0], a.w[1],
+                                                 a.w[2], t0, t1, t2);
+    if (wrap)
+      product_brick_kernel<float, true><<<bricks, 256, 0, st>>>(a, (cx<float>*)px, (cx<float>*)py, (cx<float>*)pz);
+    else
+      product_brick_kernel<float, false><<<bricks, 256, 0, st>>>(a, (cx<float>*)px, (cx<float>*)py, (cx<float>*)pz);
   } else {
-    if (wrap) rotate_product_kernel<double, true><<<grid, 256, 0, st>>>(a);
-    else rotate_product_kernel<double, false><<<grid, 256, 0, st>>>(a);
+    phase_tables_kernel<double><<<4, 256, 0, st>>>((cx<double>*)px, (cx<double>*)py, (cx<double>*)pz, a.w[0],
+                                                  a.w[1], a.w[2], t0, t1, t2);
+    if (wrap)
+      product_brick_kernel<double, true><<<bricks, 256, 0, st>>>(a, (cx<double>*)px, (cx<double>*)py,
+                                                                (cx<double>*)pz);
+    else
+      product_brick_kernel<double, false><<<bricks, 256, 0, st>>>(a, (cx<double>*)px, (cx<double>*)py,
+                                                                 (cx<double>*)pz);
   }
   GF_CUDA(cudaGetLastError());
+  GF_CUDA(cudaFreeAsync(tabs, st));
   return 0;
 }
 
@@ -432,7 +587,8 @@ int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double* domega, con
   int rc = window_operands(h1, h2, wrap, precision, (cudaStream_t)stream, &c1, &c2, w, &dim);
   if (rc) return rc;
   const int n2 = dim == 3 ? dims[2] : dims[1];
-  const bool fused = dim == 3 && (n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256 || n2 == 512);
+  static const int fuse_env = getenv("GF_FIELD_FUSED") ? atoi(getenv("GF_FIELD_FUSED")) : 0;
+  const bool fused = fuse_env && dim == 3 && (n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256 || n2 == 512);
   if (fused) {
     // pass 1 fused with the product: (w0, w1, N2) straight into work2
     rc = gf_field_zpass(h1, h2, wrap, domega, n2, R, s, precision, 0, -1, work2_dev, stream);

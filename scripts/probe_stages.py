@@ -9,6 +9,14 @@ from paper_1711_05017_b200.energy import PartAsset, score_field_device
 from paper_1711_05017_b200.spectral import forward_window, Spectrum
 
 _lib.ensure_device(0)
+
+
+def _rand_rot(seed=1):
+    q = np.random.default_rng(seed).normal(size=4)
+    w, x, y, z = q / np.linalg.norm(q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
 dev = "cuda:0"
 which = sys.argv[1:] or ["W", "F", "D", "S"]
 
@@ -42,7 +50,7 @@ if "F" in which:
         C1 = backend.DeviceWindow(torch.randn((w,) * 3, dtype=torch.complex128, device=dev))
         C2 = backend.DeviceWindow(torch.randn((w,) * 3, dtype=torch.complex128, device=dev))
         a1, a2 = FakeAsset(g, C1, w == N), FakeAsset(g, C2, w == N)
-        R = np.eye(3)
+        R = _rand_rot()
         ms = timeit(lambda: score_field_device(a1, a2, R, None, precision=prec))
         eb = 8 if prec == 32 else 16
         byt = 2 * eb * w ** 3 + eb * N ** 3

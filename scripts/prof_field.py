@@ -7,6 +7,14 @@ from paper_1711_05017_b200 import backend, _lib
 from paper_1711_05017_b200.descriptor import SampleGrid
 from paper_1711_05017_b200.energy import score_field_device
 _lib.ensure_device(0)
+
+
+def _rand_rot(seed=1):
+    q = np.random.default_rng(seed).normal(size=4)
+    w, x, y, z = q / np.linalg.norm(q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 w = int(sys.argv[2]) if len(sys.argv) > 2 else N
 g = SampleGrid(3, (N,) * 3, (-1.0,) * 3, 2.0 / N)
@@ -15,7 +23,7 @@ C2 = backend.DeviceWindow(torch.randn((w,) * 3, dtype=torch.complex128, device="
 class A:
     def __init__(s, win): s.grid, s.w = g, win
     def window(s, m=None): return s.w, w == N
-R = np.array([[0.36, 0.48, -0.8], [-0.8, 0.6, 0.0], [0.48, 0.64, 0.6]])
+R = _rand_rot()
 for _ in range(3):
     out = score_field_device(A(C1), A(C2), R, None, precision=32)
 torch.cuda.synchronize()
