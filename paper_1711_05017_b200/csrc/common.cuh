@@ -47,7 +47,9 @@ void device_free(void* p);
 // ---------------------------------------------------------------------------
 // complex arithmetic on float2/double2-shaped structs
 
-template <typename T> struct cx { T re, im; };
+// 8/16-byte aligned so that loads and stores of one element are single vector
+// accesses (a 4-byte-aligned pair splits into two LDG/STG.32).
+template <typename T> struct alignas(2 * sizeof(T)) cx { T re, im; };
 
 template <typename T> __host__ __device__ __forceinline__ cx<T> mk(T r, T i) { return cx<T>{r, i}; }
 template <typename T> __host__ __device__ __forceinline__ cx<T> operator+(cx<T> a, cx<T> b) {
