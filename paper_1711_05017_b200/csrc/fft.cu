@@ -25,12 +25,15 @@
 // the B lines are B consecutive positions of the contiguous axis -- global
 // accesses are coalesced for every axis.
 #include "../../include/geofield_b200.h"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "common.cuh"
 #include "fft_core.cuh"
 
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 
@@ -145,6 +148,287 @@ __global__ void __launch_bounds__(B*(N >= 8 ? N / 8 : 1)) fft_kernel(FftArgs a) 
     if (a.out_phase_kind) y = y * phase_factor<T>(a.out_phase_kind, a.out_phase, m);
     out[base_out + (int64_t)dst * st_out] = y;
   }
+}
+
+struct LineAddr {
+  int64_t base_in, base_out, st_in, st_out;
+  bool live;
+};
+
+// Addresses of line b of contiguous-axis tile `tile` (B lines per tile).
+template <int B>
+__device__ __forceinline__ LineAddr line_addr(const FftArgs& a, int64_t tile, int b) {
+  LineAddr L;
+  const int64_t lines = (int64_t)a.shape_in[0] * a.shape_in[1];
+  const int64_t l = tile * B + b;
+  L.live = l < lines;
+  L.base_in = l * a.shape_in[2];
+  L.base_out = l * a.shape_out[2];
+  L.st_in = 1;
+  L.st_out = 1;
+  return L;
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void store_line(const FftArgs& a, const LineAddr& L, int j, const cx<T>* line) {
+  constexpr int TPL = N / 8;
+  cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
+  const int Lout = a.shape_out[a.axis], hout = Lout / 2;
+  if (!L.live) return;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int pos = j + r * TPL;
+    int dst, m;
+    if (a.out_centered) {
+      m = pos < N / 2 ? pos : pos - N;
+      dst = m + hout;
+      if (dst < 0 || dst >= Lout) continue;
+    } else {
+      m = pos;
+      dst = pos;
+    }
+    cx<T> y = line[sidx<T>(pos)];
+    y = mk<T>(y.re * (T)a.scale, y.im * (T)a.scale);
+    if (a.out_phase_kind) y = y * phase_factor<T>(a.out_phase_kind, a.out_phase, m);
+    out[L.base_out + (int64_t)dst * L.st_out] = y;
+  }
+}
+
+// Contiguous axis, staged: a persistent CTA streams tiles of B consecutive
+// input lines (one contiguous B * Lin block) into shared memory with 1-D
+// bulk async copies (cp.async.bulk + mbarrier transaction counts), two
+// tiles ahead, so HBM reads run under the butterflies and exchanges without
+// holding registers.  Threads then read their first-stage points from the
+// staging buffer (unit stride, conflict-free).  Same semantics as fft_kernel.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+
+template <typename T, int N, int B>
+__global__ void __launch_bounds__(B * (N / 8)) fft_rows_staged_kernel(FftArgs a, int64_t ntiles) {
+  constexpr int TPL = N / 8;
+  constexpr int LD = LineLD<T, N>::value;
+  extern __shared__ __align__(128) unsigned char fft_smem[];
+  const int Lin = a.shape_in[2];
+  const int tile_elems = B * Lin;  // multiple of 2 (16-byte granules) -- checked by the launcher
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fft_smem);
+  cx<T>* stage0 = reinterpret_cast<cx<T>*>(fft_smem + 128);
+  cx<T>* lines = stage0 + 2 * tile_elems;
+  const int tid = threadIdx.x;
+  const int b = tid / TPL, j = tid % TPL;
+  const int64_t nlines = (int64_t)a.shape_in[0] * a.shape_in[1];
+  const cx<T>* __restrict__ in = reinterpret_cast<const cx<T>*>(a.in);
+  const cx<T>* __restrict__ tw = reinterpret_cast<const cx<T>*>(a.tw);
+  auto issue = [&](int64_t t, int s) {
+    const int64_t l0 = t * B;
+    const int64_t nl = nlines - l0 < B ? nlines - l0 : B;
+    bulk_load(stage0 + s * tile_elems, in + l0 * Lin, (unsigned)(nl * Lin * sizeof(cx<T>)), &bars[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  cx<T>* line = lines + b * LD;
+  const int hin = Lin / 2;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it & 1;
+    mbar_wait(&bars[s], (it >> 1) & 1);
+    const LineAddr L = line_addr<B>(a, tile, b);
+    const cx<T>* src_line = stage0 + s * tile_elems + b * Lin;
+    cx<T> v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int pos = j + r * TPL;
+      int src, m;
+      if (a.in_centered) {
+        m = pos < N / 2 ? pos : pos - N;
+        src = m + hin;
+        if (src < 0 || src >= Lin) src = -1;
+      } else {
+        m = pos;
+        src = pos;
+      }
+      cx<T> x = mk<T>(0, 0);
+      if (L.live && src >= 0) {
+        x = src_line[src];
+        if (a.in_phase_kind) x = x * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
+      }
+      v[r] = x;
+    }
+    __syncthreads();  // stage s fully read: refill it two tiles ahead
+    if (tid == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, s);
+    fft_line<T, N>(v, line, j, tw, a.sign);
+    store_line<T, N>(a, L, j, line);
+  }
+}
+
+// Strided axes, TMA-staged: a persistent CTA owns tiles of RB lines (RB
+// consecutive positions of the contiguous axis = one 128-byte row per line
+// position).  Tiles arrive by tensor-map bulk copies (3-D boxes of <= 256
+// rows) into a [row][RB] shared tile, three buffers deep, two tiles ahead;
+// the FFT runs in place in that tile (lanes walk the RB columns: every
+// exchange is a full conflict-free row); the result leaves by tensor-map
+// bulk stores.  No register staging of HBM traffic, no LSU instructions for
+// it -- the issue slots go to the butterflies.  Same semantics as fft_kernel.
+struct TmaGeom {
+  int rin, nbin;          // input box rows, boxes per tile
+  int rout;               // output box rows
+  int ptiles;             // tiles along the contiguous axis
+};
+
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap* tm, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+               "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(src))
+               : "memory");
+}
+
+template <typename T, int N>
+__global__ void __launch_bounds__((128 / sizeof(cx<T>)) * (N / 8))
+    fft_cols_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, FftArgs a,
+                        TmaGeom g, int64_t ntiles) {
+  constexpr int RB = 128 / sizeof(cx<T>);  // lines per tile (one 128-byte row)
+  constexpr int TPL = N / 8;
+  constexpr int U = sizeof(cx<T>) / 8;     // 8-byte tensor-map units per element
+  extern __shared__ __align__(128) unsigned char fft_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fft_smem);
+  cx<T>* bufs = reinterpret_cast<cx<T>*>(fft_smem + 128);
+  const int tid = threadIdx.x;
+  const int b = tid % RB, j = tid / RB;
+  const int ax = a.axis;
+  const int Lin = a.shape_in[ax], Lout = a.shape_out[ax], hin = Lin / 2, hout = Lout / 2;
+  const cx<T>* __restrict__ tw = reinterpret_cast<const cx<T>*>(a.tw);
+  const unsigned tx_bytes = (unsigned)(g.nbin * g.rin * 128);
+  auto coords = [&](int64_t t, int row, int& c0, int& c1, int& c2) {
+    const int o = (int)(t / g.ptiles), p0 = (int)(t % g.ptiles) * RB;
+    c0 = p0 * U;
+    if (ax == 1) {
+      c1 = row;
+      c2 = o;
+    } else {
+      c1 = o;
+      c2 = row;
+    }
+  };
+  auto issue_load = [&](int64_t t, int s) {
+    cx<T>* dst = bufs + (size_t)s * N * RB;
+    const unsigned bb = (unsigned)__cvta_generic_to_shared(&bars[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(tx_bytes) : "memory");
+    for (int k = 0; k < g.nbin; ++k) {
+      int c0, c1, c2;
+      coords(t, k * g.rin, c0, c1, c2);
+      tma_load3(dst + (size_t)k * g.rin * RB, &tin, c0, c1, c2, &bars[s]);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < 3; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (blockIdx.x < ntiles) issue_load(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue_load(blockIdx.x + gridDim.x, 1);
+  }
+  __syncthreads();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it % 3;
+    cx<T>* buf = bufs + (size_t)s * N * RB;
+    mbar_wait(&bars[s], (it / 3) & 1);
+    cx<T> v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int pos = j + r * TPL;
+      int src, m;
+      if (a.in_centered) {
+        m = pos < N / 2 ? pos : pos - N;
+        src = m + hin;
+        if (src < 0 || src >= Lin) src = -1;
+      } else {
+        m = pos;
+        src = pos;
+      }
+      cx<T> x = mk<T>(0, 0);
+      if (src >= 0) {
+        x = buf[src * RB + b];
+        if (a.in_phase_kind) x = x * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
+      }
+      v[r] = x;
+    }
+    fft_line<T, N, RB>(v, buf + b, j, tw, a.sign);  // ends with __syncthreads
+    if (a.scale != 1.0 || a.out_phase_kind) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int pos = j + r * TPL;
+        const int m = a.out_centered ? (pos < N / 2 ? pos : pos - N) : pos;
+        cx<T> y = buf[pos * RB + b];
+        y = mk<T>(y.re * (T)a.scale, y.im * (T)a.scale);
+        if (a.out_phase_kind) y = y * phase_factor<T>(a.out_phase_kind, a.out_phase, m);
+        buf[pos * RB + b] = y;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      // output rows: node order -> rows [0, N); centred -> dst [0, hout) from
+      // pos [N - hout, N) and dst [hout, Lout) from pos [0, Lout - hout)
+      int c0, c1, c2;
+      if (!a.out_centered) {
+        for (int r0 = 0; r0 < N; r0 += g.rout) {
+          coords(tile, r0, c0, c1, c2);
+          tma_store3(&tout, c0, c1, c2, buf + (size_t)r0 * RB);
+        }
+      } else {
+        for (int r0 = 0; r0 < hout; r0 += g.rout) {
+          coords(tile, r0, c0, c1, c2);
+          tma_store3(&tout, c0, c1, c2, buf + (size_t)(N - hout + r0) * RB);
+        }
+        for (int r0 = hout; r0 < Lout; r0 += g.rout) {
+          coords(tile, r0, c0, c1, c2);
+          tma_store3(&tout, c0, c1, c2, buf + (size_t)(r0 - hout) * RB);
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the buffer two tiles ahead held the previous tile: its store must
+      // have finished reading before the refill
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      const int64_t t2 = tile + 2 * (int64_t)gridDim.x;
+      if (t2 < ntiles) issue_load(t2, (it + 2) % 3);
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Strided axes, complex64: one thread owns the same FFT positions of two
@@ -324,6 +608,113 @@ cudaError_t launch_pair(const FftArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+bool staged_enabled() {
+  static const bool on = !getenv("GF_FFT_NOSTAGE");
+  return on;
+}
+
+template <typename T, int N, int B>
+cudaError_t launch_staged(const FftArgs& a, cudaStream_t st) {
+  const int64_t ntiles = ceil_div((int64_t)a.shape_in[0] * a.shape_in[1], B);
+  const size_t smem = 128 + sizeof(cx<T>) * ((size_t)2 * B * a.shape_in[2] + (size_t)B * LineLD<T, N>::value);
+  if (smem > 200 * 1024) return launch_nb<T, N, B>(a, st);
+  static size_t configured = 0;
+  static int per_sm = 1;
+  if (smem > configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(fft_rows_staged_kernel<T, N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int n = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fft_rows_staged_kernel<T, N, B>, B * (N / 8), smem);
+  per_sm = n > 0 ? n : 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+  fft_rows_staged_kernel<T, N, B><<<(unsigned)grid, B * (N / 8), smem, st>>>(a, ntiles);
+  return cudaGetLastError();
+}
+
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+bool tma_enabled() {
+  static const bool on = !getenv("GF_FFT_NOTMA");
+  return on;
+}
+
+// 3-D map over a (s0, s1, s2) complex array in 8-byte units; box of 128 bytes
+// along s2 and `rows` along the transform axis.
+bool encode_map(CUtensorMap* m, const void* base, const int* shape, int esz, int axis, int rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int u = esz / 8;
+  cuuint64_t dims[3] = {(cuuint64_t)shape[2] * u, (cuuint64_t)shape[1], (cuuint64_t)shape[0]};
+  cuuint64_t strides[2] = {(cuuint64_t)shape[2] * esz, (cuuint64_t)shape[1] * shape[2] * esz};
+  cuuint32_t box[3] = {16, axis == 1 ? (cuuint32_t)rows : 1u, axis == 0 ? (cuuint32_t)rows : 1u};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// returns cudaErrorNotSupported when the shape does not fit the TMA path
+template <typename T, int N>
+cudaError_t launch_tma(const FftArgs& a, cudaStream_t st) {
+  constexpr int RB = 128 / sizeof(cx<T>);
+  const int esz = sizeof(cx<T>);
+  const int Lin = a.shape_in[a.axis], Lout = a.shape_out[a.axis];
+  if (((uintptr_t)a.in & 15) || ((uintptr_t)a.out & 15)) return cudaErrorNotSupported;
+  if (((int64_t)a.shape_in[2] * esz) % 16 || ((int64_t)a.shape_out[2] * esz) % 16) return cudaErrorNotSupported;
+  if (a.out_centered && (Lout % 2)) return cudaErrorNotSupported;
+  TmaGeom g;
+  g.rin = Lin < 256 ? Lin : 256;
+  g.nbin = (Lin + g.rin - 1) / g.rin;
+  if (g.nbin * g.rin > N) return cudaErrorNotSupported;
+  g.rout = a.out_centered ? (Lout / 2 < 256 ? Lout / 2 : 256) : (N < 256 ? N : 256);
+  if (a.out_centered && (Lout / 2) % g.rout) return cudaErrorNotSupported;
+  g.ptiles = (a.shape_in[2] + RB - 1) / RB;
+  CUtensorMap tin, tout;
+  if (!encode_map(&tin, a.in, a.shape_in, esz, a.axis, g.rin)) return cudaErrorNotSupported;
+  if (!encode_map(&tout, a.out, a.shape_out, esz, a.axis, g.rout)) return cudaErrorNotSupported;
+  const int so = a.axis == 0 ? a.shape_in[1] : a.shape_in[0];
+  const int64_t ntiles = (int64_t)so * g.ptiles;
+  const size_t smem = 128 + (size_t)3 * N * 128;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fft_cols_tma_kernel<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  static int per_sm = 0;
+  if (!per_sm) {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fft_cols_tma_kernel<T, N>, RB * (N / 8), smem);
+    per_sm = n > 0 ? n : 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+  fft_cols_tma_kernel<T, N><<<(unsigned)grid, RB * (N / 8), smem, st>>>(tin, tout, a, g, ntiles);
+  return cudaGetLastError();
+}
+
 // lines per CTA: strided axes need >= 128 contiguous bytes per row per CTA
 // (B = 16 complex64 / 8 complex128) for full-sector, full-line coalescing;
 // the contiguous axis only needs enough threads (B * N / 8 >= 256).
@@ -333,7 +724,18 @@ cudaError_t launch_n(const FftArgs& a, cudaStream_t st) {
   constexpr int B_row = 128 / sizeof(cx<T>);
   constexpr int B_thr = (256 / TPL) < 1 ? 1 : (256 / TPL) > 32 ? 32 : (256 / TPL);
   constexpr int B_str = (B_row > B_thr ? B_row : B_thr) * TPL > 1024 ? 1024 / TPL : (B_row > B_thr ? B_row : B_thr);
+  if constexpr (N >= 64) {
+    if (a.axis == 2 && staged_enabled() && ((int64_t)B_thr * a.shape_in[2] * sizeof(cx<T>)) % 16 == 0 &&
+        ((uintptr_t)a.in & 15) == 0)
+      return launch_staged<T, N, B_thr>(a, st);
+  }
   if (a.axis == 2) return launch_nb<T, N, B_thr>(a, st);
+  if constexpr (N >= 64 && N <= 512) {
+    if (tma_enabled()) {
+      cudaError_t e = launch_tma<T, N>(a, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   if constexpr (sizeof(T) == 4 && N >= 64 && N <= 512) {
     if (a.shape_in[2] % 2 == 0 && a.shape_out[2] % 2 == 0 && pair_enabled()) return launch_pair<N, 16>(a, st);
   }

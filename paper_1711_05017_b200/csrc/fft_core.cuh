@@ -107,7 +107,12 @@ template <int N> struct FftShape {
 // Transform one line.  On entry v[r] holds FFT input position j + r * TPL of
 // this thread; on exit the natural-order result is in line[0..N) (all
 // threads of the line synchronised).  `line` is this line's shared buffer.
-template <typename T, int N>
+// Element i of a line: padded private line (RS = 0), or row i of a [row][RS]
+// tile whose lines are its columns (RS > 0: lanes of a warp walk the columns,
+// so every access pattern below is a full, conflict-free 128-byte row).
+template <typename T, int RS> __device__ __forceinline__ int lidx(int i) { return RS ? i * RS : sidx<T>(i); }
+
+template <typename T, int N, int RS = 0>
 __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<T>* __restrict__ tw, int sign) {
   using S = FftShape<N>;
   constexpr int TPL = S::TPL, PT = S::PT;
@@ -117,7 +122,7 @@ __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<
     if (s > 0) {
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = line[sidx<T>(j + r * TPL)];
+      for (int r = 0; r < 8; ++r) v[r] = line[lidx<T, RS>(j + r * TPL)];
     }
     const int k = j & (Ns - 1);
     if (Ns > 1) twiddle_powers<T, 8>(v, ldtw(&tw[k * (N / (Ns * 8))]));
@@ -125,7 +130,7 @@ __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<
     const int idx = (j - k) * 8 + k;
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 8; ++r) line[sidx<T>(idx + r * Ns)] = v[r];
+    for (int r = 0; r < 8; ++r) line[lidx<T, RS>(idx + r * Ns)] = v[r];
     Ns *= 8;
   }
   if constexpr (S::rest == 4 || S::rest == 2) {
@@ -134,7 +139,7 @@ __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<
     if constexpr (S::n_r8 > 0) {
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = line[sidx<T>(j + r * TPL)];
+      for (int r = 0; r < 8; ++r) v[r] = line[lidx<T, RS>(j + r * TPL)];
     }
     cx<T> w[PT];
 #pragma unroll
@@ -156,7 +161,7 @@ __device__ __forceinline__ void fft_line(cx<T>* v, cx<T>* line, int j, const cx<
       const int jj = j + q * TPL;
       const int k = jj & (Ns - 1);
 #pragma unroll
-      for (int r = 0; r < R; ++r) line[sidx<T>((jj - k) * R + k + r * Ns)] = w[q * R + r];
+      for (int r = 0; r < R; ++r) line[lidx<T, RS>((jj - k) * R + k + r * Ns)] = w[q * R + r];
     }
   }
   __syncthreads();
