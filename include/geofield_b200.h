@@ -111,6 +111,18 @@ int gf_affinity_grid(int d, const double *elems, const double *normals, const do
                      double gconst, double lam_in, double lam_out, double max_angle, int max_depth, double eta_floor,
                      void *values_dev, uint8_t *flags_dev, double *stats, void *stream);
 
+/* Slab of the same pipeline for multi-GPU node sharding:
+ * owned axis-0 planes [plane0, plane0 + nplanes) of the global grid `dims`,
+ * computed together with halo_lo / halo_hi neighbour planes so the
+ * excluded-node neighbour fill sees across the slab boundary; node
+ * coordinates use the global index (bit-identical to gf_affinity_grid).
+ * Outputs hold only the owned planes; stats cover only the owned nodes. */
+int gf_affinity_planes(int d, const double *elems, const double *normals, const double *measures, int64_t ne,
+                       const int32_t *dims, const double *origin, double spacing, int32_t plane0, int32_t nplanes,
+                       int32_t halo_lo, int32_t halo_hi, int family, double sigma, double gconst, double lam_in,
+                       double lam_out, double max_angle, int max_depth, double eta_floor, void *values_dev,
+                       uint8_t *flags_dev, double *stats, void *stream);
+
 /* Spectra (stage 2) and landscapes (stage 4) ------------------------------ */
 
 /* One batched line-FFT pass along `axis` of a 3D row-major complex array

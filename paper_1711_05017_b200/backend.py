@@ -367,3 +367,30 @@ def affinity_grid(solid, grid, family, sigma, gconst, lam_in, lam_out, max_angle
                                float(eta_floor), ctypes.c_void_p(values.data_ptr()),
                                ctypes.c_void_p(flags.data_ptr()), dptr(stats), ctypes.c_void_p(st)))
     return values, flags, (int(stats[0]), float(stats[1]))
+
+
+def affinity_planes(solid, grid, plane0, nplanes, halo_lo, halo_hi, family, sigma, gconst, lam_in, lam_out, max_angle,
+                    max_depth, eta_floor):
+    """`affinity_grid` restricted to axis-0 planes [plane0, plane0 + nplanes)
+    of `grid` (halo planes computed for the neighbour fill, not returned);
+    bit-identical to the same planes of the whole-grid result."""
+    import torch
+
+    dev = _lib.ensure_device()
+    elems, normals, measures = _elements(solid)
+    plane = int(np.prod(grid.dims[1:]))
+    m = int(nplanes) * plane
+    values = torch.empty(m, dtype=torch.complex128, device=f"cuda:{dev}")
+    flags = torch.empty(m, dtype=torch.uint8, device=f"cuda:{dev}")
+    stats = np.zeros(2)
+    dims = (ctypes.c_int32 * 3)(*(list(grid.dims) + [1] * (3 - len(grid.dims))))
+    origin = np.zeros(3)
+    origin[:grid.dimension] = grid.origin
+    st = torch.cuda.current_stream(values.device).cuda_stream
+    check(LIB.gf_affinity_planes(grid.dimension, dptr(elems), dptr(np.ascontiguousarray(normals)), dptr(measures),
+                                 len(elems), dims, dptr(origin), float(grid.spacing), int(plane0), int(nplanes),
+                                 int(halo_lo), int(halo_hi), int(family), float(sigma), float(gconst), float(lam_in),
+                                 float(lam_out), float(max_angle), int(max_depth), float(eta_floor),
+                                 ctypes.c_void_p(values.data_ptr()), ctypes.c_void_p(flags.data_ptr()), dptr(stats),
+                                 ctypes.c_void_p(st)))
+    return values, flags, (int(stats[0]), float(stats[1]))

@@ -109,6 +109,7 @@ struct PointSource {
   int dims[3];
   double origin[3];
   double spacing;
+  int x0;  // global index of local plane 0 along axis 0 (slab sharding)
   __device__ __forceinline__ void get(int64_t i, double* p) const {
     if (P) {
       for (int a = 0; a < d; ++a) p[a] = P[i * d + a];
@@ -119,13 +120,13 @@ struct PointSource {
       int64_t r = i / dims[2];
       int j = (int)(r % dims[1]);
       int ii = (int)(r / dims[1]);
-      p[0] = node_coord(origin[0], spacing, ii);
+      p[0] = node_coord(origin[0], spacing, ii + x0);
       p[1] = node_coord(origin[1], spacing, j);
       p[2] = node_coord(origin[2], spacing, k);
     } else {
       int j = (int)(i % dims[1]);
       int ii = (int)(i / dims[1]);
-      p[0] = node_coord(origin[0], spacing, ii);
+      p[0] = node_coord(origin[0], spacing, ii + x0);
       p[1] = node_coord(origin[1], spacing, j);
     }
   }
@@ -530,20 +531,29 @@ int gf_sweep(int d, const double* elems, const double* normals, const double* me
   return 0;
 }
 
-int gf_affinity_grid(int d, const double* elems, const double* normals, const double* measures, int64_t ne,
-                     const int32_t* dims, const double* origin, double spacing, int family, double sigma,
-                     double gconst, double lam_in, double lam_out, double max_angle, int max_depth, double eta_floor,
-                     void* values_dev, uint8_t* flags_dev, double* stats, void* stream) {
+int gf_affinity_planes(int d, const double* elems, const double* normals, const double* measures, int64_t ne,
+                       const int32_t* dims, const double* origin, double spacing, int32_t plane0, int32_t nplanes,
+                       int32_t halo_lo, int32_t halo_hi, int family, double sigma, double gconst, double lam_in,
+                       double lam_out, double max_angle, int max_depth, double eta_floor, void* values_dev,
+                       uint8_t* flags_dev, double* stats, void* stream) {
   int rc = check_dim(d);
   if (rc) return rc;
   GF_CHECK(elems && normals && measures && dims && origin && values_dev && flags_dev && stats && ne > 0, GF_EINVAL,
            "bad argument");
   GF_CHECK(max_depth >= 0 && max_depth <= 24, GF_EINVAL, "max_depth must be in [0, 24]");
+  GF_CHECK(nplanes > 0 && plane0 >= 0 && plane0 + nplanes <= dims[0], GF_EINVAL, "plane range outside the grid");
+  GF_CHECK(halo_lo >= 0 && halo_hi >= 0 && plane0 - halo_lo >= 0 && plane0 + nplanes + halo_hi <= dims[0], GF_EINVAL,
+           "halo outside the grid");
   cudaStream_t st = (cudaStream_t)stream;
   const int E = d == 3 ? 9 : 4;
-  int64_t m = 1;
-  for (int a = 0; a < d; ++a) m *= dims[a];
-  DevBuf de, dn, dm, dxi, dwind, dxe, dip, dres, dcl, dval;
+  int64_t plane = 1;
+  for (int a = 1; a < d; ++a) plane *= dims[a];
+  const int lo = plane0 - halo_lo, cnt = nplanes + halo_lo + halo_hi;
+  const int64_t m = (int64_t)cnt * plane;          // nodes computed (owned + halo planes)
+  const int64_t own = (int64_t)nplanes * plane;    // nodes returned
+  const int64_t off = (int64_t)halo_lo * plane;    // first owned node in the computed block
+  const bool halos = halo_lo || halo_hi;
+  DevBuf de, dn, dm, dxi, dwind, dxe, dip, dres, dcl, dval, hval, hflg;
   if ((rc = upload(elems, sizeof(double) * E * ne, de, st))) return rc;
   if ((rc = upload(normals, sizeof(double) * d * ne, dn, st))) return rc;
   if ((rc = upload(measures, sizeof(double) * ne, dm, st))) return rc;
@@ -555,6 +565,15 @@ int gf_affinity_grid(int d, const double* elems, const double* normals, const do
   GF_CUDA(cudaMalloc(&dval.p, sizeof(double) * 2 * m));
   GF_CUDA(cudaMemsetAsync(dres.p, 0, sizeof(double) * m, st));
   GF_CUDA(cudaMemsetAsync(dcl.p, 0, sizeof(int64_t) * m, st));
+  // with halo planes, fill a full computed block and hand back the owned part
+  void* out_vals = values_dev;
+  uint8_t* out_flags = flags_dev;
+  if (halos) {
+    GF_CUDA(cudaMalloc(&hval.p, sizeof(double) * 2 * m));
+    GF_CUDA(cudaMalloc(&hflg.p, m));
+    out_vals = hval.p;
+    out_flags = (uint8_t*)hflg.p;
+  }
   PointSource src = {};
   src.P = nullptr;
   src.d = d;
@@ -562,6 +581,8 @@ int gf_affinity_grid(int d, const double* elems, const double* normals, const do
     src.dims[a] = a < d ? dims[a] : 1;
     src.origin[a] = a < d ? origin[a] : 0.0;
   }
+  src.dims[0] = cnt;
+  src.x0 = lo;
   src.spacing = spacing;
   const double eta_min = eta_floor * spacing;
   unsigned grid = (unsigned)ceil_div(m, kThreads);
@@ -588,15 +609,21 @@ int gf_affinity_grid(int d, const double* elems, const double* normals, const do
   }
   combine_kernel<<<148 * 8, 256, 0, st>>>(m, (const double*)dxi.p, (const double*)dwind.p, (const double*)dip.p,
                                           (const double*)dres.p, family, lam_in, lam_out, eta_min, max_angle,
-                                          (double*)dval.p, flags_dev);
+                                          (double*)dval.p, out_flags);
   GF_CUDA(cudaGetLastError());
   neighbor_fill_kernel<<<148 * 8, 256, 0, st>>>(d, src.dims[0], src.dims[1], d == 3 ? src.dims[2] : 1,
-                                                (const double*)dval.p, flags_dev, (double*)values_dev);
+                                                (const double*)dval.p, out_flags, (double*)out_vals);
   GF_CUDA(cudaGetLastError());
+  if (halos) {
+    GF_CUDA(cudaMemcpyAsync(values_dev, (const double*)out_vals + 2 * off, sizeof(double) * 2 * own,
+                            cudaMemcpyDeviceToDevice, st));
+    GF_CUDA(cudaMemcpyAsync(flags_dev, out_flags + off, own, cudaMemcpyDeviceToDevice, st));
+  }
   DevBuf dst;
   GF_CUDA(cudaMalloc(&dst.p, 2 * sizeof(unsigned long long)));
   GF_CUDA(cudaMemsetAsync(dst.p, 0, 2 * sizeof(unsigned long long), st));
-  stats_kernel<<<148 * 4, 256, 0, st>>>((const double*)dres.p, (const int64_t*)dcl.p, m, (unsigned long long*)dst.p);
+  stats_kernel<<<148 * 4, 256, 0, st>>>((const double*)dres.p + off, (const int64_t*)dcl.p + off, own,
+                                        (unsigned long long*)dst.p);
   GF_CUDA(cudaGetLastError());
   unsigned long long hs[2];
   GF_CUDA(cudaMemcpyAsync(hs, dst.p, sizeof hs, cudaMemcpyDeviceToHost, st));
@@ -604,6 +631,16 @@ int gf_affinity_grid(int d, const double* elems, const double* normals, const do
   stats[0] = (double)hs[0];
   stats[1] = __longlong_as_double_host(hs[1]);
   return 0;
+}
+
+int gf_affinity_grid(int d, const double* elems, const double* normals, const double* measures, int64_t ne,
+                     const int32_t* dims, const double* origin, double spacing, int family, double sigma,
+                     double gconst, double lam_in, double lam_out, double max_angle, int max_depth, double eta_floor,
+                     void* values_dev, uint8_t* flags_dev, double* stats, void* stream) {
+  GF_CHECK(dims != nullptr, GF_EINVAL, "bad argument");
+  return gf_affinity_planes(d, elems, normals, measures, ne, dims, origin, spacing, 0, dims[0], 0, 0, family, sigma,
+                            gconst, lam_in, lam_out, max_angle, max_depth, eta_floor, values_dev, flags_dev, stats,
+                            stream);
 }
 
 }  // extern "C"

@@ -10,6 +10,11 @@
   the data by output y-slabs (each rank gets every x-plane of its y-range),
   and the last pass inverts along x (w0 -> N0).  Rank r ends with the
   landscape rows y in [c_r, d_r): an (N0, d_r - c_r, N2) slab.
+* Density (D1/D2): node slabs along axis 0, one per rank, triangles
+  replicated; each rank also computes one halo plane per interior side so
+  the excluded-node neighbour fill is exact across slab boundaries (the
+  halo is computed, not exchanged: no collective on the data path).  Counts
+  and flags are reduced once at the end.
 * The single haptic query does not shard: replicas only.
 
 The decomposition logic (ranges, split sizes, re-assembly) is host code that
@@ -203,3 +208,75 @@ def _pass(x, out_shape, axis, n, scale, precision):
     _lib.check(_lib.LIB.gf_fft_pass(precision, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), si, so,
                                     axis, n, 1, 0, 1, 0.0, 0.0, float(scale), ctypes.c_void_p(st)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# density node slabs
+
+
+def density_slab_plan(n0, world):
+    """Per rank: (plane0, nplanes, halo_lo, halo_hi) over axis 0."""
+    plan = []
+    for r in range(world):
+        lo, hi = shard_range(n0, r, world)
+        plan.append((lo, hi - lo, 1 if 0 < lo < hi else 0, 1 if lo < hi < n0 else 0))
+    return plan
+
+
+def affinity_field_slab(solid, grid, spec, policy=None, group=None, gather=True, compute=None):
+    """affinity_field with the grid's axis-0 planes sharded across ranks.
+
+    Each rank runs the GPU pipeline on its slab (gf_affinity_planes: global
+    node indexing, halo planes for the neighbour fill), so every node's
+    value and flag is bit-identical to the single-GPU affinity_field.
+    gather=True returns the full ComplexField on every rank; otherwise
+    (local values (nplanes * plane,), plane range, local flags, stats).
+    `compute(solid, grid, plane0, nplanes, halo_lo, halo_hi)` may replace
+    the GPU call (tests drive the decomposition on CPU)."""
+    import torch
+
+    from .descriptor import ComplexField, IntegrationPolicy, _check_grid, _unit_constant
+
+    policy = policy or IntegrationPolicy()
+    _check_grid(solid, grid)
+    rank, world = _world(group)
+    plane0, n, hlo, hhi = density_slab_plan(grid.dims[0], world)[rank]
+    plane = int(np.prod(grid.dims[1:]))
+    family = 0 if spec.family == "InverseSquare" else 1
+    if compute is None:
+        def compute(solid, grid, p0, np_, lo, hi):
+            return backend.affinity_planes(solid, grid, p0, np_, lo, hi, family, spec.sigma,
+                                           _unit_constant(grid.dimension), spec.lambda_in, spec.lambda_out,
+                                           policy.max_solid_angle, policy.max_recursion_depth, policy.eta_floor)
+    if n > 0:
+        values, fb, (nclamp, worst) = compute(solid, grid, plane0, n, hlo, hhi)
+    else:
+        values = torch.empty(0, dtype=torch.complex128)
+        fb = torch.empty(0, dtype=torch.uint8)
+        nclamp, worst = 0, 0.0
+    fb_h = fb.cpu().numpy()
+    excluded, unresolved, inside = (fb_h & 1) != 0, (fb_h & 2) != 0, (fb_h & 4) != 0
+    local_flags = (np.flatnonzero(excluded | unresolved) + plane0 * plane).tolist()
+    counts = torch.tensor([int(excluded.sum()), int(unresolved.sum()), int(inside.sum()), int(nclamp)],
+                          dtype=torch.float64)
+    worst_t = torch.tensor([float(worst)], dtype=torch.float64)
+    flags = local_flags
+    if world > 1:
+        dist = _dist()
+        dev = values.device if values.is_cuda else torch.device("cpu")
+        if dist.get_backend(group) == "nccl":
+            counts, worst_t = counts.to(dev), worst_t.to(dev)
+        dist.all_reduce(counts, group=group)
+        dist.all_reduce(worst_t, op=dist.ReduceOp.MAX, group=group)
+        if gather:
+            parts = [None] * world
+            dist.all_gather_object(parts, local_flags, group=group)
+            flags = [f for p in parts for f in p]  # ranks own increasing plane ranges: already sorted
+    c = counts.cpu().numpy()
+    stats = {"excluded": int(c[0]), "eta_clamped": int(c[3]),
+             "worst_residual": float(worst_t.cpu()[0]) if family else 0.0,
+             "unresolved_nodes": int(c[1]), "inside_nodes": int(c[2])}
+    if not gather:
+        return values, (plane0, plane0 + n), local_flags, stats
+    full = gather_rows(values.reshape(n, plane), grid.dims[0], group).reshape(-1)
+    return ComplexField(grid, full, flags=flags, stats=stats)

@@ -100,3 +100,30 @@ def test_affinity_deterministic_and_inverse_square():
     want = oracle.neighbor_average(wind.astype(np.complex128), oracle.distance(ico.element_arrays()[0],
                                                                                g.points()) < 0.25 * g.spacing, g.dims)
     np.testing.assert_allclose(inv.values, want, atol=1e-12)
+
+
+@pytest.mark.parametrize("scene,n", [("peg3d", 32), ("peg2d", 64)])
+def test_node_slabs_bit_identical_to_whole_grid(scene, n):
+    """The multi-GPU node-slab path (gf_affinity_planes with halo planes, one
+    call per rank) reassembles to exactly the single-GPU field."""
+    import torch
+
+    from paper_1711_05017_b200 import parallel
+    from paper_1711_05017_b200.descriptor import _unit_constant
+
+    sc = scenes.get_scene(scene)
+    g = sc.grid(n)
+    pol = IntegrationPolicy()
+    args = (1, KERNEL.sigma, _unit_constant(g.dimension), KERNEL.lambda_in, KERNEL.lambda_out, pol.max_solid_angle,
+            pol.max_recursion_depth, pol.eta_floor)
+    v0, f0, (c0, w0) = backend.affinity_grid(sc.fixed, g, *args)
+    for world in (2, 3, 5):
+        vs, fs, cl, wr = [], [], 0, 0.0
+        for p0, k, lo, hi in parallel.density_slab_plan(g.dims[0], world):
+            v, f, (c, w) = backend.affinity_planes(sc.fixed, g, p0, k, lo, hi, *args)
+            vs.append(v)
+            fs.append(f)
+            cl += c
+            wr = max(wr, w)
+        assert torch.equal(torch.cat(vs), v0) and torch.equal(torch.cat(fs), f0)
+        assert cl == c0 and wr == w0

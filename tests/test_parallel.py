@@ -16,7 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1711_05017_b200 import parallel
+from paper_1711_05017_b200 import parallel, scenes
+from paper_1711_05017_b200.descriptor import KernelSpec, SampleGrid
 
 
 def _free_port():
@@ -94,8 +95,40 @@ def _worker(rank, world, port, results):
         full = oracle.score_field(C1, C2, False, N, origin, h, R)
         ylo, yhi = y_r[rank]
         results[f"field{rank}"] = float(np.max(np.abs(land - full[:, ylo:yhi])) / np.max(np.abs(full)))
+        # --- density node slabs: halo planes make the neighbour fill exact
+        g = SampleGrid(3, (8, 8, 8), (-0.8, -0.8, -0.8), 0.2)
+        solid = scenes.box_mesh((0.2, 0.2, 0.2))
+        got = parallel.affinity_field_slab(solid, g, KernelSpec(), compute=_fake_planes)
+        want_v, want_fb, (want_cl, want_w) = _fake_planes(solid, g, 0, g.dims[0], 0, 0)
+        wfb = want_fb.numpy()
+        ok = (np.array_equal(got.values, want_v.numpy()) and
+              got.flags == np.flatnonzero((wfb & 3) != 0).tolist() and
+              got.stats["excluded"] == int(((wfb & 1) != 0).sum()) and
+              got.stats["inside_nodes"] == int(((wfb & 4) != 0).sum()) and
+              got.stats["eta_clamped"] == want_cl and got.stats["worst_residual"] == want_w)
+        results[f"density{rank}"] = bool(ok)
     finally:
         dist.destroy_process_group()
+
+
+def _fake_planes(solid, grid, p0, n, lo, hi):
+    """Deterministic stand-in for gf_affinity_planes: per-node values from
+    global coordinates, an excluded set, and the neighbour fill over the
+    computed block (owned + halo planes), returning the owned planes."""
+    a, b = p0 - lo, p0 + n + hi
+    idx = np.stack(np.meshgrid(np.arange(a, b), *[np.arange(m) for m in grid.dims[1:]], indexing="ij"), -1)
+    x = np.asarray(grid.origin) + grid.spacing * idx
+    raw = np.sin(3 * x[..., 0]) + 1j * np.cos(x[..., 1] * x[..., 2] + x[..., 0])
+    ex = raw.real > 0.6
+    unres = (idx.sum(-1) % 5) == 0
+    inside = raw.imag > 0.5
+    dims = (b - a,) + tuple(grid.dims[1:])
+    vals = oracle.neighbor_average(raw.ravel(), ex.ravel(), dims).reshape(dims)
+    fb = (ex.astype(np.uint8) | (unres.astype(np.uint8) << 1) | (inside.astype(np.uint8) << 2))
+    own = slice(lo, lo + n)
+    resid = np.abs(raw[own]).ravel()
+    return (torch.from_numpy(vals[own].ravel().copy()), torch.from_numpy(fb[own].ravel().copy()),
+            (int(unres[own].sum()), float(resid.max())))
 
 
 @pytest.mark.parametrize("world", [2])
@@ -106,6 +139,18 @@ def test_sweep_and_slab_decomposition_gloo(world):
     for r in range(world):
         assert results[f"sweep{r}"] <= 1e-12
         assert results[f"field{r}"] <= 1e-12
+        assert results[f"density{r}"]
+
+
+def test_density_slab_plan():
+    for n0 in (4, 8, 9, 64):
+        for world in (1, 2, 3, 8):
+            plan = parallel.density_slab_plan(n0, world)
+            assert sum(p[1] for p in plan) == n0
+            for p0, n, lo, hi in plan:
+                assert p0 - lo >= 0 and p0 + n + hi <= n0
+                if n:
+                    assert lo == (1 if p0 > 0 else 0) and hi == (1 if p0 + n < n0 else 0)
 
 
 def test_shard_range_partitions():
