@@ -10,6 +10,10 @@
   the data by output y-slabs (each rank gets every x-plane of its y-range),
   and the last pass inverts along x (w0 -> N0).  Rank r ends with the
   landscape rows y in [c_r, d_r): an (N0, d_r - c_r, N2) slab.
+* Forward window (W1) of a node-sharded field: the z and y passes (pruned
+  N -> w) run on each rank's x-planes, one all-to-all re-slices the
+  (nx, w, w) planes into window y-slabs, and the x pass (N0 -> w) finishes;
+  only the (2K)^3 window ever crosses the fabric.
 * Density (D1/D2): node slabs along axis 0, one per rank, triangles
   replicated; each rank also computes one halo plane per interior side so
   the excluded-node neighbour fill is exact across slab boundaries (the
@@ -280,3 +284,62 @@ def affinity_field_slab(solid, grid, spec, policy=None, group=None, gather=True,
         return values, (plane0, plane0 + n), local_flags, stats
     full = gather_rows(values.reshape(n, plane), grid.dims[0], group).reshape(-1)
     return ComplexField(grid, full, flags=flags, stats=stats)
+
+
+# ---------------------------------------------------------------------------
+# forward window of a node-sharded field
+
+
+def _wpass(x, out_shape, axis, n, scale, precision):
+    """One pruned forward pass: node-ordered in, DC-centred window out with
+    the (-1)^m centre phase (spectral.forward_window's per-axis pass)."""
+    import torch
+
+    out = torch.empty(out_shape, dtype=x.dtype, device=x.device)
+    if x.numel() == 0 or out.numel() == 0:
+        return out
+    si = (ctypes.c_int32 * 3)(*x.shape)
+    so = (ctypes.c_int32 * 3)(*out_shape)
+    st = torch.cuda.current_stream(x.device).cuda_stream
+    _lib.check(_lib.LIB.gf_fft_pass(precision, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), si, so,
+                                    axis, n, 0, 1, -1, 0.0, 0.5, float(scale), ctypes.c_void_p(st)))
+    return out
+
+
+def window_inner_passes(local, dims, w, precision=64):
+    """z then y pass of a rank's (nx, N1, N2) field planes -> (nx, w, w)."""
+    nx = local.shape[0]
+    a = _wpass(local, (nx, dims[1], w), 2, dims[2], 1.0, precision)
+    return _wpass(a, (nx, w, w), 1, dims[1], 1.0, precision)
+
+
+def window_outer_pass(slab, dims, w, cell_volume, precision=64):
+    """x pass of a (N0, wy, w) window y-slab -> (w, wy, w), scaled by dV."""
+    return _wpass(slab, (w, slab.shape[1], w), 0, dims[0], cell_volume, precision)
+
+
+def forward_window_slab(local, grid, w, precision=64, group=None, gather=True):
+    """spectral.forward_window for a field sharded by axis-0 planes
+    (shard_range layout, local = this rank's (nx, N1, N2) CUDA complex
+    planes).  Bit-identical to the single-GPU window: the same 1-D passes on
+    the same data, with one all-to-all between the y and x passes.  Returns
+    the full (w, w, w) window on every rank (gather) or this rank's window
+    y-slab (w, wy, w) and its range."""
+    import torch
+
+    if grid.dimension != 3:
+        raise ValueError("slab decomposition is for 3D fields")
+    rank, world = _world(group)
+    N = list(grid.dims)
+    dtype = torch.complex128 if precision == 64 else torch.complex64
+    local = local.reshape(-1, N[1], N[2]).to(dtype)
+    x_r = [shard_range(N[0], r, world) for r in range(world)]
+    wy_r = [shard_range(w, r, world) for r in range(world)]
+    b = window_inner_passes(local, N, w, precision)
+    slab = exchange_planes_to_slabs(torch.view_as_real(b), x_r, wy_r, rank, group)
+    slab = torch.view_as_complex(slab.contiguous())
+    out = window_outer_pass(slab, N, w, grid.cell_volume, precision)
+    if not gather:
+        return out, wy_r[rank]
+    full = gather_rows(torch.view_as_real(out.permute(1, 0, 2).contiguous()), w, group)
+    return torch.view_as_complex(full.contiguous()).permute(1, 0, 2).contiguous()
