@@ -174,6 +174,11 @@ int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double *domega, con
 int gf_measure_fma_peak(int precision, double *tflops);
 /* Launch-overhead probe: host and device microseconds per empty launch. */
 int gf_measure_launch(int n, int blocks, double *host_us, double *dev_us);
+/* Host<->device round trips (diagnostics for the query path): out[0] launch +
+ * mapped completion p50 us, out[1] pre-enqueued kernel released by a mapped
+ * flag (cuStreamWaitValue32) p50 us, out[2] GPU read latency of mapped host
+ * memory ns, out[3] mapped write + system fence ns. */
+int gf_measure_roundtrip(int n, double *out);
 
 /* Persistent haptic server (Q1 latency path): a resident grid serves one
  * query per call through a host-mapped mailbox -- no kernel launch per

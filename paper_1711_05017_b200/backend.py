@@ -179,14 +179,20 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
     d = W1.ndim
     q = _qb
     arg = q.arg
-    Rf = np.asarray(R, dtype=np.float64).reshape(-1)
-    arg[: d * d] = Rf
-    arg[9: 9 + d] = t_eff
-    arg[12: 12 + d] = center
-    arg[15: 15 + d] = domega
+    if d == 3:
+        arg[:9] = R.ravel() if type(R) is np.ndarray else np.asarray(R, dtype=np.float64).ravel()
+        arg[9:12] = t_eff
+        arg[12:15] = center
+        arg[15:18] = domega
+    else:
+        arg[:4] = np.asarray(R, dtype=np.float64).ravel()
+        arg[9:11] = t_eff
+        arg[12:14] = center
+        arg[15:17] = domega
+        arg[14] = arg[17] = 0.0
     bits = 64 if (precision or _precision) == "fp64" else 32
     srv = _servers.get((W1.handle, W2.handle, bool(wrap), bits)) if _servers else None
-    if srv is not None and srv.matches(dcell, arg[15: 15 + d], arg[12: 12 + d]):
+    if srv is not None and srv.dcell == dcell and arg[12:18].tobytes() == srv.cd_bytes:
         rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
     else:
         rc = LIB.gf_cascade_fast(W1.handle, W2.handle, 1 if wrap else 0, q.pd, float(dcell), q.pR, q.pt, q.pc, bits,
@@ -225,6 +231,9 @@ class HapticServer:
                                   dptr(self.center), self.bits, float(idle_timeout_s), ctypes.byref(sid)))
         self.id = sid.value
         self.key = (self.W1.handle, self.W2.handle, self.wrap, self.bits)
+        cd = np.zeros(6)  # center (3) | domega (3), as laid out in the query buffer
+        cd[:d], cd[3:3 + d] = self.center, self.dom
+        self.cd_bytes = cd.tobytes()
         _servers[self.key] = self
 
     def matches(self, dcell, dom, center):

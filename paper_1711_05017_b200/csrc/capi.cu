@@ -84,7 +84,7 @@ static Window* find_window(uint64_t h) {
 struct Context {
   int device = -1;
   cudaStream_t stream = nullptr;
-  double* host_out = nullptr;     // pinned + mapped: 14 doubles, then the completion word at [16]
+  unsigned long long* host_out = nullptr;  // pinned + mapped: 28 self-tagged result slots (CascadeArgs::ll_out)
   unsigned long long seq = 0;
   // cached launch arguments of the last single query (same windows/grid)
   bool cached = false;
@@ -92,7 +92,7 @@ struct Context {
   int cwrap = -1, cprec = 0;
   double cdom[3] = {0, 0, 0}, cdcell = 0, ccen[3] = {0, 0, 0};
   CascadeArgs cargs;
-  double* dev_out_alias = nullptr;
+  unsigned long long* dev_out_alias = nullptr;
   double* partials = nullptr;
   unsigned* counters = nullptr;
   int64_t partials_cap = 0, counters_cap = 0;
@@ -111,7 +111,8 @@ static int ensure_context() {
   int lo = 0, hi = 0;
   GF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   GF_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi));
-  GF_CUDA(cudaHostAlloc((void**)&c.host_out, 64 * sizeof(double), cudaHostAllocMapped));
+  GF_CUDA(cudaHostAlloc((void**)&c.host_out, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
+  std::memset(c.host_out, 0, 64 * sizeof(unsigned long long));
   GF_CUDA(cudaHostGetDevicePointer((void**)&c.dev_out_alias, c.host_out, 0));
   c.device = dev;
   return 0;
@@ -213,6 +214,30 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
   a.variant = g_variant;
   a.tile_force = g_tile;
   a.debug = g_debug;
+  return 0;
+}
+
+// Poll the 28 self-tagged result slots until every one carries `seq`, then
+// unpack the 14 doubles.  `alive` is checked every ~64k spins (returns
+// non-zero when the producer can no longer answer).
+template <typename Alive>
+static int wait_ll(const volatile unsigned long long* slots, unsigned long long seq, double* res, Alive alive) {
+  const unsigned tag = (unsigned)seq;
+  unsigned spins = 0;
+  while (true) {
+    bool ok = true;
+    for (int i = 0; i < 28 && ok; ++i) ok = (unsigned)(slots[i] >> 32) == tag;
+    if (ok) break;
+    if ((++spins & 0xffff) == 0) {
+      int rc = alive();
+      if (rc) return rc;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  for (int i = 0; i < 14; ++i) {
+    const unsigned long long bits = (slots[2 * i] & 0xffffffffull) | (slots[2 * i + 1] << 32);
+    std::memcpy(&res[i], &bits, sizeof(double));
+  }
   return 0;
 }
 
@@ -361,8 +386,10 @@ int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double 
     if (rc) return rc;
     a.partials = c.partials;
     a.counters = c.counters;
-    a.out = c.dev_out_alias;
-    a.done_flag = a.single ? reinterpret_cast<volatile unsigned long long*>(c.dev_out_alias + 16) : nullptr;
+    // lone-query kernel: self-tagged result slots; other plans (non-default
+    // variants): plain doubles into the same mapped buffer + stream sync
+    a.ll_out = a.single ? c.dev_out_alias : nullptr;
+    a.out = a.single ? nullptr : reinterpret_cast<double*>(c.dev_out_alias);
     c.cargs = a;
     c.ch1 = h1;
     c.ch2 = h2;
@@ -376,30 +403,32 @@ int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double 
   CascadeArgs& a = c.cargs;
   embed_pose(d, R, t_eff, a.pose_inline);
   a.done_seq = ++c.seq;
-  GF_CUDA(launch_cascade(a, 1, c.stream));
-  if (a.done_flag) {
-    // poll the mapped completion word (no driver call on the fast path);
-    // fall back to a stream sync after ~1 s so a failed kernel surfaces
-    volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(c.host_out + 16);
+  double res[14];
+  if (a.ll_out) {
+    GF_CUDA(launch_cascade(a, 1, c.stream));
+    // poll the self-tagged result slots (no driver call on the fast path);
+    // after ~1 s of silence fall back to a stream sync so a failed kernel surfaces
     auto t0 = std::chrono::steady_clock::now();
-    unsigned spins = 0;
-    while (*flag != a.done_seq) {
-      if ((++spins & 0xffff) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(1)) {
-        GF_CUDA(cudaStreamSynchronize(c.stream));
-        GF_CHECK(*flag == a.done_seq, GF_EINTERNAL, "query kernel finished without publishing its result");
-        break;
-      }
-    }
-    std::atomic_thread_fence(std::memory_order_acquire);
+    rc = wait_ll(c.host_out, a.done_seq, res, [&]() -> int {
+      if (std::chrono::steady_clock::now() - t0 < std::chrono::seconds(1)) return 0;
+      GF_CUDA(cudaStreamSynchronize(c.stream));
+      const unsigned tag = (unsigned)a.done_seq;
+      for (int i = 0; i < 28; ++i)
+        GF_CHECK((unsigned)(c.host_out[i] >> 32) == tag, GF_EINTERNAL, "query kernel finished without its result");
+      return 0;
+    });
+    if (rc) return rc;
   } else {
+    GF_CUDA(launch_cascade(a, 1, c.stream));
     GF_CUDA(cudaStreamSynchronize(c.stream));
+    std::memcpy(res, c.host_out, 14 * sizeof(double));
   }
   if (d == 3) {
-    std::memcpy(out, c.host_out, 14 * sizeof(double));
+    std::memcpy(out, res, 14 * sizeof(double));
   } else {  // [S, Tx, Ty, Gz]
-    std::memcpy(out, c.host_out, 6 * sizeof(double));
-    out[6] = c.host_out[12];
-    out[7] = c.host_out[13];
+    std::memcpy(out, res, 6 * sizeof(double));
+    out[6] = res[12];
+    out[7] = res[13];
   }
   return 0;
 }
@@ -461,13 +490,9 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
 // persistent haptic server
 
 namespace {
-struct Mailbox {               // host-mapped, one per server
-  volatile unsigned long long seq;
-  volatile unsigned stop;
-  unsigned pad;
-  double pose[12];
-  double out[16];
-  volatile unsigned long long done;
+struct Mailbox {  // host-mapped, one per server (see ServerCtl / CascadeArgs::ll_out)
+  volatile unsigned long long req[32];  // kReqSlots self-tagged request slots
+  volatile unsigned long long out[32];  // 28 self-tagged result slots
 };
 struct Server {
   int device = 0;
@@ -475,7 +500,7 @@ struct Server {
   cudaStream_t stream = nullptr;
   Mailbox* mb = nullptr;       // host view
   Mailbox* mb_dev = nullptr;   // device alias
-  void* dev_words = nullptr;   // dev_seq (8 B) + dev_pose (96 B)
+  void* dev_words = nullptr;   // device copy of the request slots (forwarded by CTA 0)
   double* partials = nullptr;
   unsigned* counters = nullptr;
   unsigned long long seq = 0;
@@ -491,11 +516,23 @@ Server* find_server(uint64_t id) {
   return it == g_servers.end() ? nullptr : it->second.get();
 }
 
+void post_request(Server* s, const double* pose12, unsigned stop) {
+  const unsigned long long tag = (unsigned long long)(unsigned)(++s->seq) << 32;
+  unsigned long long halves[24];
+  std::memcpy(halves, pose12, 12 * sizeof(double));
+  for (int i = 0; i < 12; ++i) {
+    unsigned long long bits;
+    std::memcpy(&bits, pose12 + i, 8);
+    s->mb->req[2 * i] = tag | (bits & 0xffffffffull);
+    s->mb->req[2 * i + 1] = tag | (bits >> 32);
+  }
+  s->mb->req[kReqSlots - 1] = tag | stop;
+}
+
 int stop_server(Server* s) {
   if (!s->running) return 0;
-  s->mb->stop = 1u;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  s->mb->seq = ++s->seq;
+  const double zero[12] = {};
+  post_request(s, zero, 1u);
   GF_CUDA(cudaStreamSynchronize(s->stream));
   s->running = false;
   server_stopped();
@@ -525,22 +562,19 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, do
   GF_CUDA(cudaHostAlloc((void**)&s->mb, sizeof(Mailbox), cudaHostAllocMapped));
   std::memset((void*)s->mb, 0, sizeof(Mailbox));
   GF_CUDA(cudaHostGetDevicePointer((void**)&s->mb_dev, (void*)s->mb, 0));
-  GF_CUDA(cudaMalloc(&s->dev_words, 8 + 12 * sizeof(double)));
-  GF_CUDA(cudaMemsetAsync(s->dev_words, 0, 8 + 12 * sizeof(double), s->stream));
+  GF_CUDA(cudaMalloc(&s->dev_words, 32 * sizeof(unsigned long long)));
+  GF_CUDA(cudaMemsetAsync(s->dev_words, 0, 32 * sizeof(unsigned long long), s->stream));
   GF_CUDA(cudaMalloc((void**)&s->partials, (size_t)a.blocks_per_pose * kNumMoments * sizeof(double)));
   GF_CUDA(cudaMalloc((void**)&s->counters, sizeof(unsigned)));
   GF_CUDA(cudaMemsetAsync(s->counters, 0, sizeof(unsigned), s->stream));
   a.partials = s->partials;
   a.counters = s->counters;
-  a.out = s->mb_dev->out;
-  a.done_flag = &s->mb_dev->done;
-  a.debug = nullptr;
+  a.out = nullptr;
+  a.ll_out = const_cast<unsigned long long*>(s->mb_dev->out);
+  a.debug = g_debug;  // null unless gf_set_cascade_debug armed it
   ServerCtl ctl;
-  ctl.host_seq = &s->mb_dev->seq;
-  ctl.host_stop = &s->mb_dev->stop;
-  ctl.host_pose = s->mb_dev->pose;
-  ctl.dev_seq = (volatile unsigned long long*)s->dev_words;
-  ctl.dev_pose = (double*)((char*)s->dev_words + 8);
+  ctl.host_req = s->mb_dev->req;
+  ctl.dev_req = (volatile unsigned long long*)s->dev_words;
   ctl.start_seq = 0;
   ctl.idle_timeout_ns = (unsigned long long)((idle_timeout_s > 0 ? idle_timeout_s : 30.0) * 1e9);
   auto tl0 = std::chrono::steady_clock::now();
@@ -563,33 +597,31 @@ int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, do
   Server* s = find_server(server_id);
   GF_CHECK(s && R && t_eff && out, GF_EINVAL, "unknown server or null argument");
   GF_CHECK(s->running, GF_EINVAL, "server is not running (stopped or idle-timed out)");
-  embed_pose(s->d, R, t_eff, s->mb->pose);
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  const unsigned long long seq = ++s->seq;
-  s->mb->seq = seq;
+  double pose[12];
+  embed_pose(s->d, R, t_eff, pose);
+  post_request(s, pose, 0u);
+  const unsigned long long seq = s->seq;
+  double res[14];
   auto t0 = std::chrono::steady_clock::now();
-  unsigned spins = 0;
-  while (s->mb->done != seq) {
-    if ((++spins & 0xffff) == 0) {
-      cudaError_t e = cudaStreamQuery(s->stream);
-      if (e != cudaErrorNotReady) {  // kernel exited (idle timeout) or failed
-        s->running = false;
-        server_stopped();
-        if (e != cudaSuccess) GF_CUDA(e);
-        GF_CHECK(s->mb->done == seq, GF_EINVAL, "server exited (idle timeout); start a new one");
-        break;
-      }
-      GF_CHECK(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(5), GF_EINTERNAL,
-               "haptic server did not answer within 5 s");
+  int rc = wait_ll(s->mb->out, seq, res, [&]() -> int {
+    cudaError_t e = cudaStreamQuery(s->stream);
+    if (e != cudaErrorNotReady) {  // kernel exited (idle timeout) or failed
+      s->running = false;
+      server_stopped();
+      if (e != cudaSuccess) GF_CUDA(e);
+      GF_CHECK(false, GF_EINVAL, "server exited (idle timeout); start a new one");
     }
-  }
-  std::atomic_thread_fence(std::memory_order_acquire);
+    GF_CHECK(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(5), GF_EINTERNAL,
+             "haptic server did not answer within 5 s");
+    return 0;
+  });
+  if (rc) return rc;
   if (s->d == 3) {
-    std::memcpy(out, s->mb->out, 14 * sizeof(double));
+    std::memcpy(out, res, 14 * sizeof(double));
   } else {
-    std::memcpy(out, s->mb->out, 6 * sizeof(double));
-    out[6] = s->mb->out[12];
-    out[7] = s->mb->out[13];
+    std::memcpy(out, res, 6 * sizeof(double));
+    out[6] = res[12];
+    out[7] = res[13];
   }
   return 0;
 }

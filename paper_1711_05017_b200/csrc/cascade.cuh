@@ -40,8 +40,12 @@ struct CascadeArgs {
   unsigned* counters;    // n_poses, zero-initialised, re-armed by the kernel
   double* out;           // n_poses * 14 (interleaved complex128 x 7)
   unsigned long long* debug;  // optional per-block phase timestamps (single kernel)
-  volatile unsigned long long* done_flag;  // single kernel: host-mapped completion word (or null)
-  unsigned long long done_seq;            // value stored there after the outputs
+  // single kernel, host-polled result: 28 host-mapped 8-byte slots, slot 2i+h
+  // = (seq32 << 32) | 32-bit half h of output i.  Each slot is one atomic
+  // 8-byte store carrying its own validity tag, so the host needs no separate
+  // completion word and the kernel no system-scope fence (or null: `out`).
+  unsigned long long* ll_out;
+  unsigned long long done_seq;  // tag of this query
 };
 
 // 26 moment accumulators (layout = the moment index order used by finalize)
@@ -69,12 +73,13 @@ template <typename T> struct Acc26 {
 };
 
 // Persistent haptic server mailbox plumbing (cascade_single.cu)
+// Persistent server mailbox: kReqSlots 8-byte slots, (seq32 << 32) | payload:
+// slots 0..23 the 32-bit halves of the pose (R row-major, then t_eff), slot
+// 24 the stop word.  A request is complete when every slot carries its tag.
+constexpr int kReqSlots = 25;
 struct ServerCtl {
-  volatile unsigned long long* host_seq;   // host-mapped: request sequence number
-  volatile unsigned* host_stop;            // host-mapped: stop request
-  const volatile double* host_pose;        // host-mapped: R (9) + t_eff (3)
-  volatile unsigned long long* dev_seq;    // device: forwarded sequence number
-  double* dev_pose;                        // device: forwarded pose
+  const volatile unsigned long long* host_req;  // host-mapped request slots
+  volatile unsigned long long* dev_req;         // device copy forwarded by CTA 0
   unsigned long long start_seq;
   unsigned long long idle_timeout_ns;
 };

@@ -28,7 +28,7 @@ namespace gf {
 namespace {
 
 constexpr int kThreads = 256;
-int g_cluster = 2;  // CTAs per cluster (DSMEM reduction stage); 1 disables
+int g_cluster = 4;  // CTAs per cluster (DSMEM reduction stage); 1 disables
 
 struct SinglePose {
   double mu[3][3];
@@ -41,6 +41,44 @@ struct SinglePose {
   double kt[3];        // T_a  = 2 pi i kt[a] Z_a        (= dw_a)
   long long ufix[3][4];  // fixed-point u_a = ufix[a][3] + sum_b ufix[a][b] kappa_b
 };
+
+// Cluster stage state (shared memory of every CTA; used in rank 0): the
+// other ranks push their 26 block moments into `gather` with DSMEM stores
+// and arrive on `bar` (release.cluster); rank 0 waits on it (acquire) -- a
+// one-way hand-off, no cluster-wide barrier on the query path.
+constexpr int kMaxCluster = 8;
+struct ClusterRed {
+  double gather[kMaxCluster][kNumMoments];
+  unsigned long long bar;
+  unsigned parity;  // phase of `bar` for the next query
+  int armed;        // 1 until the start-of-kernel cluster barrier has been waited on
+};
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned map_rank0(unsigned addr) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(addr));
+  return r;
+}
+
+// Kernel start: rank 0 initialises the hand-off barrier; every CTA arrives
+// (relaxed) on the cluster barrier and waits for it lazily before its first
+// push, so the init is visible without a barrier on the critical path.
+__device__ __forceinline__ void cluster_red_init(ClusterRed& cr) {
+  unsigned crank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  if (threadIdx.x == 0) {
+    cr.parity = 0;
+    cr.armed = 1;
+    if (crank == 0 && csize > 1) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&cr.bar)), "r"(csize - 1));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  if (csize > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
 
 __device__ __forceinline__ double exact_u_s(const double* R, const double* dom, int a, int kx, int ky, int kz,
                                             int hx, int hy, int hz, int ha) {
@@ -76,12 +114,28 @@ __device__ __forceinline__ double finalize_slot(const CascadeArgs& a, const Sing
   return dc * acc;
 }
 
+// Result of one query: slot i of 14 to `out`, or as two self-tagged 8-byte
+// words to the host-mapped LL slots (plain stores, no fence: the host checks
+// the tags).
+__device__ __forceinline__ void emit_output(const CascadeArgs& a, int i, double v, unsigned long long seq) {
+  if (a.ll_out) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long tag = (seq & 0xffffffffull) << 32;
+    volatile unsigned long long* o = a.ll_out;
+    o[2 * i] = tag | (bits & 0xffffffffull);
+    o[2 * i + 1] = tag | (bits >> 32);
+  } else {
+    a.out[i] = v;
+  }
+}
+
 // One pose over all retained modes, spread across the grid; shared state is
 // passed in so the same body runs in the one-shot kernel and in the
 // persistent haptic server.  Non-final blocks return early (block-uniform).
 template <typename T, bool WRAP>
 __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const double* src, SinglePose& sp, double* red,
-                                                 unsigned& ticket, unsigned char* smem_raw) {
+                                                 unsigned& ticket, ClusterRed& cr, unsigned char* smem_raw,
+                                                 unsigned long long done_seq) {
   using P4 = typename pair4<T>::type;
   // dynamic: transpose buffer tr[26][257] (reduction) | px | py | pz
   T(*tr)[kThreads + 1] = reinterpret_cast<T(*)[kThreads + 1]>(smem_raw);
@@ -296,27 +350,52 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   if (c < kNumMoments && s == 0) red[c] = part;
   __syncthreads();
 
-  double* out = a.out;
   const int bpp = gridDim.x;
   if (bpp == 1) {
-    if (tid < 14) out[tid] = finalize_slot(a, sp, red, tid);
+    if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
     return;
   }
   GF_STAMP(3)
-  // ---- cluster stage: rank 0 of each 8-CTA cluster sums its cluster's
-  // block moments through distributed shared memory (fixed rank order)
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const unsigned crank = cluster.block_rank(), csize = cluster.num_blocks();
+  // ---- cluster stage: ranks 1.. push their block moments to rank 0 through
+  // distributed shared memory; rank 0 sums them in rank order (fixed)
+  unsigned crank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
   const int cid = blockIdx.x / (int)csize, nclusters = gridDim.x / (int)csize;
-  cluster.sync();
-  if (crank == 0 && tid < kNumMoments) {
-    double v = 0.0;
-    for (unsigned r = 0; r < csize; ++r) v += cluster.map_shared_rank(red, r)[tid];
-    a.partials[(int64_t)tid * nclusters + cid] = v;  // moment-major
+  if (csize > 1) {
+    if (cr.armed) {  // rank 0's barrier init is visible once the start barrier completes
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      if (tid == 0) cr.armed = 0;
+    }
+    if (crank != 0) {
+      if (tid < kNumMoments)
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(map_rank0(smem_addr(&cr.gather[crank][tid]))),
+                     "d"(red[tid])
+                     : "memory");
+      __syncthreads();
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(map_rank0(smem_addr(&cr.bar)))
+                     : "memory");
+      return;
+    }
+    if (tid < kNumMoments) {
+      const unsigned bar = smem_addr(&cr.bar), par = cr.parity;
+      unsigned done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(par)
+            : "memory");
+      double v = red[tid];
+      for (unsigned r = 1; r < csize; ++r) v += cr.gather[r][tid];
+      a.partials[(int64_t)tid * nclusters + cid] = v;  // moment-major
+    }
+    __syncthreads();
+    if (tid == 0) cr.parity ^= 1u;
+  } else if (tid < kNumMoments) {
+    a.partials[(int64_t)tid * nclusters + cid] = red[tid];
   }
-  cluster.sync();  // keep the other ranks' shared memory alive until read
-  if (crank != 0) return;
   // ---- grid stage: integer ticket with release/acquire ordering
   __syncthreads();
   if (tid == 0) {
@@ -343,15 +422,8 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   for (int o = 4; o > 0; o >>= 1) part2 += __shfl_down_sync(0xffffffffu, part2, o, 8);
   if (c < kNumMoments && s == 0) red[c] = part2;
   __syncthreads();
-  if (tid < 14) out[tid] = finalize_slot(a, sp, red, tid);
+  if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
   if (tid == 0) a.counters[0] = 0u;
-  if (a.done_flag) {  // publish completion to the polling host thread
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence_system();
-      *a.done_flag = a.done_seq;
-    }
-  }
   GF_STAMP(5)
 }
 
@@ -361,8 +433,15 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   __shared__ SinglePose sp;
   __shared__ double red[kNumMoments];
   __shared__ unsigned ticket;
-  const double* src = a.poses ? a.poses + a.pose_offset * 12 : a.pose_inline;
-  single_pose_body<T, WRAP>(a, src, sp, red, ticket, smem_raw);
+  __shared__ ClusterRed cr;
+  __shared__ double pose_s[12];
+  // pose to shared memory with direct (constant-bank) parameter reads: a
+  // generic pointer into the parameter block turns every use into a global
+  // load of freshly written launch memory on the setup critical path
+  if (threadIdx.x < 12)
+    pose_s[threadIdx.x] = a.poses ? a.poses[a.pose_offset * 12 + threadIdx.x] : a.pose_inline[threadIdx.x];
+  cluster_red_init(cr);  // ends with __syncthreads
+  single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, a.done_seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -381,53 +460,60 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   __shared__ unsigned ticket;
   __shared__ unsigned long long cur;
   __shared__ double pose_s[12];
+  __shared__ ClusterRed cr;
+  cluster_red_init(cr);
   unsigned long long last = ctl.start_seq;
+  const int tid = threadIdx.x;
   while (true) {
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-      // warp 0 of block 0: lane 0 polls the host mailbox; then the pose and
-      // stop word are fetched by 13 lanes in parallel (one PCIe round trip)
-      const int lane = threadIdx.x;
-      unsigned long long sq = 0;
-      if (lane == 0) {
-        unsigned long long t0, t1;
+    const unsigned expect = (unsigned)(last + 1);
+    if (tid < 32) {
+      // warp 0: lanes 0..24 read the 25 request slots in one instruction and
+      // the warp votes; CTA 0 polls the host mailbox (one PCIe round trip per
+      // poll, the pose arrives with the tags) and forwards the slots to device
+      // memory, the other CTAs poll that copy in L2
+      const int lane = tid;
+      unsigned long long v = 0;
+      bool ok;
+      if (blockIdx.x == 0) {
+        unsigned long long t0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        while ((sq = *ctl.host_seq) == last) {
+        while (true) {
+          if (lane < kReqSlots) v = ctl.host_req[lane];
+          ok = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
+          if (ok) break;
+          unsigned long long t1;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-          if (t1 - t0 > ctl.idle_timeout_ns) {
-            sq = kServerStop;
+          if (t1 - t0 > ctl.idle_timeout_ns) {  // idle: forward a stop request
+            v = lane == kReqSlots - 1 ? (((unsigned long long)expect << 32) | 1ull)
+                                      : ((unsigned long long)expect << 32);
             break;
           }
         }
-        __threadfence_system();
+        if (lane < kReqSlots) ctl.dev_req[lane] = v;
+      } else {
+        while (true) {
+          if (lane < kReqSlots) v = ctl.dev_req[lane];
+          ok = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
+          if (ok) break;
+          __nanosleep(20);
+        }
       }
-      sq = __shfl_sync(0xffffffffu, sq, 0);
-      unsigned stop = 0;
-      if (sq != kServerStop) {
-        if (lane < 12) ctl.dev_pose[lane] = ctl.host_pose[lane];
-        if (lane == 12) stop = *ctl.host_stop;
-      }
-      stop = __shfl_sync(0xffffffffu, stop, 12);
-      if (stop) sq = kServerStop;
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) {
-        *ctl.dev_seq = sq;
-        cur = sq;
-      }
-    } else if (blockIdx.x != 0 && threadIdx.x == 0) {
-      unsigned long long sq;
-      while ((sq = *ctl.dev_seq) == last) __nanosleep(32);
-      __threadfence();
-      cur = sq;
+      // halves -> pose doubles (lanes 2i, 2i+1 -> pose_s[i]); stop word
+      const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, (2 * lane) & 31);
+      const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)v, (2 * lane + 1) & 31);
+      const unsigned stopw = __shfl_sync(0xffffffffu, (unsigned)v, kReqSlots - 1);
+      if (lane < 12) pose_s[lane] = __hiloint2double((int)hi, (int)lo);
+      if (lane == 0) cur = stopw ? kServerStop : last + 1;
     }
     __syncthreads();
     const unsigned long long sq = cur;
     if (sq == kServerStop) break;
-    if (threadIdx.x < 12) pose_s[threadIdx.x] = __ldcg(ctl.dev_pose + threadIdx.x);  // bypass stale L1
-    __syncthreads();
-    CascadeArgs q = a;
-    q.done_seq = sq;
-    single_pose_body<T, WRAP>(q, pose_s, sp, red, ticket, smem_raw);
+    if (a.debug && tid == 0) {  // when this CTA saw the query
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      a.debug[(int64_t)blockIdx.x * 8 + 7] = t_;
+    }
+    single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, sq);
     last = sq;
     __syncthreads();
   }
@@ -475,6 +561,8 @@ int single_blocks(const CascadeArgs& a, int sms) {
   int64_t b = best < target ? best : target;
   if (best > target) b = best / ceil_div(best, target);
   if (const char* env = getenv("GF_SINGLE_CLUSTER")) g_cluster = atoi(env);  // experiments only
+  if (g_cluster < 1) g_cluster = 1;
+  if (g_cluster > kMaxCluster) g_cluster = kMaxCluster;
   b = (b / g_cluster) * g_cluster;  // whole clusters
   return (int)(b < g_cluster ? g_cluster : b);
 }

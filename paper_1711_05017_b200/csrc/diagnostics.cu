@@ -8,6 +8,7 @@
 #include "common.cuh"
 
 #include <chrono>
+#include <cstring>
 
 namespace gf {
 namespace {
@@ -99,6 +100,118 @@ extern "C" int gf_measure_launch(int n, int blocks, double* host_us, double* dev
   *dev_us = 1e3 * ms / n;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Host <-> device round-trip probe for the single-query path design.
+namespace gf {
+namespace {
+__global__ void signal_kernel(volatile unsigned* done, unsigned v) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    __threadfence_system();
+    *done = v;
+  }
+}
+// dependent reads of a host-mapped word, and mapped write + system fence
+__global__ void pcie_latency_kernel(volatile unsigned* hostw, int n, unsigned long long* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long t0, t1, t2;
+  unsigned acc = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int i = 0; i < n; ++i) acc += hostw[acc & 1];
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  for (int i = 0; i < n; ++i) {
+    hostw[2] = acc + i;
+    __threadfence_system();
+  }
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+  out[0] = (t1 - t0) / n;
+  out[1] = (t2 - t1) / n;
+  out[2] = acc;
+}
+}  // namespace
+}  // namespace gf
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <vector>
+
+// out[0]: p50 us, launch of a 1-CTA kernel that signals a mapped word, host polls
+// out[1]: p50 us, the same kernel pre-enqueued behind cuStreamWaitValue32 on a
+//         mapped flag; the host writes the flag and polls (launch off the path)
+// out[2]: GPU read latency of host-mapped memory, ns (dependent reads)
+// out[3]: GPU mapped write + __threadfence_system, ns
+extern "C" int gf_measure_roundtrip(int n, double* out) {
+  using namespace gf;
+  GF_CHECK(out && n > 0, GF_EINVAL, "bad argument");
+  cudaStream_t st;
+  GF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  unsigned* h = nullptr;
+  GF_CUDA(cudaHostAlloc((void**)&h, 4096, cudaHostAllocMapped));
+  std::memset(h, 0, 4096);
+  unsigned* d = nullptr;
+  GF_CUDA(cudaHostGetDevicePointer((void**)&d, h, 0));
+  volatile unsigned* done = h;       // word 0: completion
+  volatile unsigned* flag = h + 32;  // word 32: go flag (own line)
+  std::vector<double> t(n);
+  for (int i = 0; i < n + 50; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    signal_kernel<<<1, 32, 0, st>>>(d, (unsigned)(i + 1));
+    while (*done != (unsigned)(i + 1)) {
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    if (i >= 50) t[i - 50] = std::chrono::duration<double, std::micro>(t1 - t0).count();
+  }
+  std::sort(t.begin(), t.end());
+  out[0] = t[n / 2];
+  void* fnp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  out[1] = -1.0;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fnp, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess && fnp) {
+    auto wait = (PFN_cuStreamWaitValue32_v11070)fnp;
+    GF_CUDA(cudaStreamSynchronize(st));
+    *done = 0;
+    unsigned base = 1000;
+    auto arm = [&](unsigned k) -> int {
+      if (wait((CUstream)st, (CUdeviceptr)(d + 32), k, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) return 1;
+      signal_kernel<<<1, 32, 0, st>>>(d, k);
+      return 0;
+    };
+    GF_CHECK(arm(base + 1) == 0, GF_EINTERNAL, "cuStreamWaitValue32 failed");
+    for (int i = 0; i < n + 50; ++i) {
+      const unsigned k = base + 1 + i;
+      // let the pre-armed pair reach the wait before timing
+      auto tw = std::chrono::steady_clock::now();
+      while (std::chrono::steady_clock::now() - tw < std::chrono::microseconds(30)) {
+      }
+      auto t0 = std::chrono::steady_clock::now();
+      *flag = k;
+      while (*done != k) {
+      }
+      auto t1 = std::chrono::steady_clock::now();
+      if (i >= 50) t[i - 50] = std::chrono::duration<double, std::micro>(t1 - t0).count();
+      GF_CHECK(arm(k + 1) == 0, GF_EINTERNAL, "cuStreamWaitValue32 failed");
+    }
+    *flag = base + n + 100;  // release the last armed pair
+    GF_CUDA(cudaStreamSynchronize(st));
+    std::sort(t.begin(), t.end());
+    out[1] = t[n / 2];
+  }
+  unsigned long long* dl = nullptr;
+  GF_CUDA(cudaMalloc(&dl, 3 * sizeof(unsigned long long)));
+  pcie_latency_kernel<<<1, 32, 0, st>>>(d + 64, 200, dl);
+  unsigned long long hl[3];
+  GF_CUDA(cudaMemcpyAsync(hl, dl, sizeof hl, cudaMemcpyDeviceToHost, st));
+  GF_CUDA(cudaStreamSynchronize(st));
+  out[2] = (double)hl[0];
+  out[3] = (double)hl[1];
+  cudaFree(dl);
+  cudaFreeHost(h);
   cudaStreamDestroy(st);
   return 0;
 }

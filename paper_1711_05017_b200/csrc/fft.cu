@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(B*(N >= 8 ? N / 8 : 1)) fft_kernel(FftArgs a) 
   constexpr int TPL = FftShape<N>::TPL;  // threads per line
   constexpr int PT = FftShape<N>::PT;    // points per thread
   constexpr int LD = LineLD<T, N>::value;  // padded line stride
-  extern __shared__ __align__(16) unsigned char fft_smem[];
+  extern __shared__ __align__(128) unsigned char fft_smem[];
   cx<T>* buf = reinterpret_cast<cx<T>*>(fft_smem);
   const int tid = threadIdx.x;
   const int ax = a.axis;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(B / 2 * (N / 8), 2) fft_pair_kernel(FftArgs a)
   constexpr int TPL = N / 8;
   constexpr int LD = LineLD<T, N>::value;
   constexpr int BP = B / 2;
-  extern __shared__ __align__(16) unsigned char fft_smem[];
+  extern __shared__ __align__(128) unsigned char fft_smem[];
   cx<T>* buf = reinterpret_cast<cx<T>*>(fft_smem);
   const int tid = threadIdx.x;
   const int ax = a.axis;
