@@ -28,6 +28,10 @@ namespace gf {
 namespace {
 
 constexpr int kThreads = 256;
+// transpose row stride: = 8 (mod 32) so the reduction's reads -- lanes (c, s)
+// at c * kTrLd + s + 8 i -- hit 32 distinct banks (fp32) / distinct 8-byte
+// slots per half-warp (fp64)
+constexpr int kTrLd = kThreads + 8;
 int g_cluster = 4;  // CTAs per cluster (DSMEM reduction stage); 1 disables
 
 struct SinglePose {
@@ -138,8 +142,8 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
                                                  unsigned long long done_seq) {
   using P4 = typename pair4<T>::type;
   // dynamic: transpose buffer tr[26][257] (reduction) | px | py | pz
-  T(*tr)[kThreads + 1] = reinterpret_cast<T(*)[kThreads + 1]>(smem_raw);
-  cx<T>* ptab = reinterpret_cast<cx<T>*>(smem_raw + sizeof(T) * kNumMoments * (kThreads + 1) + 16);
+  T(*tr)[kTrLd] = reinterpret_cast<T(*)[kTrLd]>(smem_raw);
+  cx<T>* ptab = reinterpret_cast<cx<T>*>(smem_raw + sizeof(T) * kNumMoments * kTrLd + 16);
 
   const int tid = threadIdx.x;
   unsigned long long* dbg = a.debug ? a.debug + (int64_t)blockIdx.x * 8 : nullptr;
@@ -237,7 +241,14 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   Acc26<T> acc;
   acc.zero();
   GF_STAMP(1)
-  for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+  // each CTA takes a contiguous run of units: consecutive kr planes of one
+  // (p, q) patch, whose rotated C2 footprints overlap -> L1 reuse across the
+  // CTA's iterations (GF_SINGLE_ORDER=0: round-robin, for comparison)
+  const int upb = (units + gridDim.x - 1) / gridDim.x;
+  const int u_begin = a.tile == 0 ? blockIdx.x * upb : blockIdx.x;
+  const int u_step = a.tile == 0 ? 1 : gridDim.x;
+  const int u_end = a.tile == 0 ? min(units, u_begin + upb) : units;
+  for (int unit = u_begin; unit < u_end; unit += u_step) {
     const int kr = unit % wr;
     const int iq = (unit / wr) % sp.nQ;
     const int ip = unit / (wr * sp.nQ);
@@ -330,17 +341,18 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
 #pragma unroll
   for (int c = 0; c < kNumMoments; ++c) tr[c][tid] = acc.v[c];
   __syncthreads();
-  // 26 moments x 8 segments of 32 values: thread (c, s) sums its segment
+  // 26 moments x 8 interleaved strands of 32 values: thread (c, s) sums
+  // tr[c][s + 8 i], i < 32 (conflict-free, see kTrLd), fixed order
   double part = 0.0;
   const int c = tid >> 3, s = tid & 7;
   if (c < kNumMoments) {
-    T q0 = (T)0, q1 = (T)0, q2 = (T)0, q3 = (T)0;  // 4 independent chains, fixed order
+    T q0 = (T)0, q1 = (T)0, q2 = (T)0, q3 = (T)0;  // 4 independent chains
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
-      q0 += tr[c][s * 32 + i];
-      q1 += tr[c][s * 32 + i + 1];
-      q2 += tr[c][s * 32 + i + 2];
-      q3 += tr[c][s * 32 + i + 3];
+      q0 += tr[c][s + 8 * i];
+      q1 += tr[c][s + 8 * (i + 1)];
+      q2 += tr[c][s + 8 * (i + 2)];
+      q3 += tr[c][s + 8 * (i + 3)];
     }
     part = (double)((q0 + q1) + (q2 + q3));
   }
@@ -521,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
 
 template <typename T, bool WRAP>
 cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
-  size_t smem = sizeof(T) * kNumMoments * (kThreads + 1) + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
+  size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
   static size_t configured = 0;
   if (smem > configured && smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(cascade3d_single_kernel<T, WRAP>,
@@ -569,7 +581,7 @@ int single_blocks(const CascadeArgs& a, int sms) {
 
 template <typename T, bool WRAP>
 cudaError_t launch_server_t(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st) {
-  size_t smem = sizeof(T) * kNumMoments * (kThreads + 1) + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
+  size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(cascade3d_server_kernel<T, WRAP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -582,6 +594,25 @@ cudaError_t launch_server_t(const CascadeArgs& a, const ServerCtl& ctl, cudaStre
                                                                 smem);
   if (e != cudaSuccess) return e;
   if ((int64_t)per_sm * sms < a.blocks_per_pose) return cudaErrorCooperativeLaunchTooLarge;
+  // co-residency guaranteed (cooperative) and the same CTA clusters as the
+  // one-shot kernel (DSMEM hand-off stage)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.blocks_per_pose);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = g_cluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, cascade3d_server_kernel<T, WRAP>, a, ctl);
+  if (e == cudaSuccess) return e;
+  (void)cudaGetLastError();  // clusters + cooperative refused: plain cooperative launch
   CascadeArgs aa = a;
   ServerCtl cc = ctl;
   void* args[] = {&aa, &cc};
