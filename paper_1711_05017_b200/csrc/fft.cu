@@ -626,9 +626,13 @@ cudaError_t launch_staged(const FftArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  int n = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fft_rows_staged_kernel<T, N, B>, B * (N / 8), smem);
-  per_sm = n > 0 ? n : 1;
+  static size_t occ_smem = 0;
+  if (occ_smem != smem) {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fft_rows_staged_kernel<T, N, B>, B * (N / 8), smem);
+    per_sm = n > 0 ? n : 1;
+    occ_smem = smem;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

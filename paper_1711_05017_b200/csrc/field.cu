@@ -313,11 +313,10 @@ cudaError_t launch_zpass_w(const ZArgs& a, cudaStream_t st) {
 // gathered V * phase goes through shared memory and the C1 read and Q write
 // are done in z-fastest order, coalesced.  fp32 indices in 32.32 fixed point.
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a, const cx<T>* __restrict__ ptx,
-                                                            const cx<T>* __restrict__ pty,
-                                                            const cx<T>* __restrict__ ptz) {
+__global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
   using P4 = typename pair4<T>::type;
   __shared__ cx<T> sq[8 * 73];
+  __shared__ cx<T> ph[3][8];  // exp(2 pi i dw_a s_a (k_a - h_a)) for this brick's 8 modes per axis
   const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
   const int nbz = (w2 + 7) / 8, nby = (w1 + 7) / 8;
@@ -329,6 +328,17 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a, const cx<
   cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
   const T eps = (T)a.tie_eps;
   const int pf = a.perm[0], pm = a.perm[1];
+  if (t < 24) {  // float64 argument reduction, as the reference's per-axis phase (energy.py:339-341)
+    const int ax = t >> 3, o = t & 7;
+    const int k = ax == 0 ? a.kx0 + bx * 8 + o : (ax == 1 ? by * 8 + o : bz * 8 + o);
+    const int h = ax == 0 ? hx : (ax == 1 ? hy : hz);
+    double cyc = a.dom[ax] * a.s[ax] * (double)(k - h);
+    cyc -= rint(cyc);
+    double sn, cs;
+    sincospi(2.0 * cyc, &sn, &cs);
+    ph[ax][o] = mk<T>((T)cs, (T)sn);
+  }
+  __syncthreads();
   // C1 for the epilogue's (z-fastest) modes, issued before the gathers
   cx<T> c1v[2];
 #pragma unroll
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a, const cx<
       cx<T> a11 = lerp(mk<T>(e01.z, e01.w), mk<T>(e11.z, e11.w), fu);
       V = lerp(lerp(a00, a10, fv), lerp(a01, a11, fv), fs);
     }
-    sq[ox * 73 + oy * 9 + oz] = V * ((ptx[kx] * pty[ky]) * ptz[kz]);
+    sq[ox * 73 + oy * 9 + oz] = V * ((ph[0][ox] * ph[1][oy]) * ph[2][oz]);
   }
   __syncthreads();
 #pragma unroll
@@ -477,34 +487,15 @@ int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double* d
     a.perm[1] = pm;
     a.perm[2] = 3 - pf - pm;
   }
-  // separable phase tables exp(2 pi i kappa_a dw_a s_a)
-  const size_t esz = precision == 32 ? 8 : 16;
-  void* tabs = nullptr;
-  GF_CUDA(cudaMallocAsync(&tabs, esz * (a.w[0] + a.w[1] + a.w[2]), st));
-  void* px = tabs;
-  void* py = (char*)tabs + esz * a.w[0];
-  void* pz = (char*)tabs + esz * (a.w[0] + a.w[1]);
-  const double t0 = a.dom[0] * a.s[0], t1 = a.dom[1] * a.s[1], t2 = a.dom[2] * a.s[2];
   const unsigned bricks = (unsigned)(ceil_div(a.nkx, 8) * ceil_div(a.w[1], 8) * ceil_div(a.w[2], 8));
   if (precision == 32) {
-    phase_tables_kernel<float><<<4, 256, 0, st>>>((cx<float>*)px, (cx<float>*)py, (cx<float>*)pz, a.w[0], a.w[1],
-                                                 a.w[2], t0, t1, t2);
-    if (wrap)
-      product_brick_kernel<float, true><<<bricks, 256, 0, st>>>(a, (cx<float>*)px, (cx<float>*)py, (cx<float>*)pz);
-    else
-      product_brick_kernel<float, false><<<bricks, 256, 0, st>>>(a, (cx<float>*)px, (cx<float>*)py, (cx<float>*)pz);
+    if (wrap) product_brick_kernel<float, true><<<bricks, 256, 0, st>>>(a);
+    else product_brick_kernel<float, false><<<bricks, 256, 0, st>>>(a);
   } else {
-    phase_tables_kernel<double><<<4, 256, 0, st>>>((cx<double>*)px, (cx<double>*)py, (cx<double>*)pz, a.w[0],
-                                                  a.w[1], a.w[2], t0, t1, t2);
-    if (wrap)
-      product_brick_kernel<double, true><<<bricks, 256, 0, st>>>(a, (cx<double>*)px, (cx<double>*)py,
-                                                                (cx<double>*)pz);
-    else
-      product_brick_kernel<double, false><<<bricks, 256, 0, st>>>(a, (cx<double>*)px, (cx<double>*)py,
-                                                                 (cx<double>*)pz);
+    if (wrap) product_brick_kernel<double, true><<<bricks, 256, 0, st>>>(a);
+    else product_brick_kernel<double, false><<<bricks, 256, 0, st>>>(a);
   }
   GF_CUDA(cudaGetLastError());
-  GF_CUDA(cudaFreeAsync(tabs, st));
   return 0;
 }
 
