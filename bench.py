@@ -392,7 +392,8 @@ def run_engine(args):
                     "launch_path": "same call without a session: one single-query kernel launch per call"},
             "roofline": {"bound": "fp32" if prec == "fp32" else "fp64", "achieved": achieved,
                          "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value,
-                         "traffic": None,
+                         "traffic": _traffic("cascade3d_single_kernel"),
+                         "traffic_unit": "bytes per launch (DRAM read+write, ncu capture; windows stay L2-resident)",
                          "work": f"240 flops x live modes ({live:.3f} x {W ** 3}) per launch",
                          "peak_source": "FMA-chain kernel measured in this run (gf_measure_fma_peak)"},
             "cpu_baseline": cpu,
@@ -420,6 +421,22 @@ def _peaks():
             return _json.load(fh)
     except OSError:
         return {"hbm_gbs": 6650.0, "note": "fallback (B200_PROFILING.md)"}
+
+
+def _traffic(kernel):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu capture summary
+    (profiles/r01_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as fh:
+            return json.load(fh)[kernel]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def _field_traffic():
+    parts = [_traffic(k) for k in ("product_brick_kernel", "fft_rows_staged_kernel", "fft_cols_tma_kernel",
+                                   "fft_cols_tma_kernel")]
+    return None if None in parts else sum(parts)
 
 
 def _time_ms(fn, reps=3):
@@ -490,7 +507,9 @@ def measure_stages(args, rank, world, fp32_peak):
         "poses_per_s": len(ts) / (ms * 1e-3), "e2e_poses_per_s": len(ts) / e2e_s,
         "e2e_path": "parallel.pose_sweep: host poses in, host complex128 results out",
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "work": f"240 flop x live modes ({live:.3f} of m')"},
+                     "frac": achieved / fp32_peak, "work": f"240 flop x live modes ({live:.3f} of m')",
+                     "traffic": _traffic("cascade3d_kernel"),
+                     "traffic_unit": "bytes per 2048-pose launch (ncu capture)"},
         "projected_1e6_poses_s": 1e6 / (len(ts) / (ms * 1e-3)),
     }
     if rank == 0 and not args.no_cpu:
@@ -522,7 +541,9 @@ def measure_stages(args, rank, world, fp32_peak):
         "voxels_per_s": n4 ** 3 / (ms * 1e-3), "ms": ms,
         "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                      "frac": alg / (ms * 1e-3) / 1e9 / hbm, "work": "24 B/voxel algorithmic",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                     "traffic": _field_traffic(),
+                     "traffic_unit": "bytes per landscape: product + 3 FFT passes (ncu capture, 512^3)"},
         "scaling_plan": "slab-decomposed across ranks with one all-to-all (parallel.score_field_slab)",
     }
     if rank == 0 and not args.no_cpu:
