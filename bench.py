@@ -576,7 +576,8 @@ def measure_stages(args, rank, world, fp32_peak):
     sess.run(R5[:50], t5[:50], rate_hz=1000.0)  # warm
     run = sess.run(R5, t5, rate_hz=1000.0)
     out["haptic_C5"] = {"workload": f"bolt-nut 256^3 grid, K=64 (w=128, m'={w5 ** 3}), {frames}-frame screw "
-                                    "trajectory (2 turns, pitch 0.1) paced at 1 kHz, one evaluate per frame, fp32",
+                                    "trajectory (2 turns, pitch 0.1) paced at 1 kHz, one evaluate per frame served by a "
+                                    "resident query grid (haptic_session), fp32",
                         **run, "budget_us": 1000.0}
     del f5, sess
     torch.cuda.empty_cache()
@@ -606,9 +607,12 @@ def measure_stages(args, rank, world, fp32_peak):
     gd = sc.grid(64)
     affinity_field(sc.fixed, gd, sc.kernel)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    fd = affinity_field(sc.fixed, gd, sc.kernel)
-    dt = time.perf_counter() - t0
+    dt = None
+    for _ in range(3):  # best of 3 wall-clock calls (host allocation jitter)
+        t0 = time.perf_counter()
+        fd = affinity_field(sc.fixed, gd, sc.kernel)
+        d1 = time.perf_counter() - t0
+        dt = d1 if dt is None else min(dt, d1)
     nf = len(sc.fixed.mesh.faces)
     out["density_D"] = {"workload": f"affinity_field, bored block ({nf} faces) on 64^3, float64 bit-exact flags",
                         "voxels_per_s": gd.node_count / dt, "node_face_pairs_per_s": gd.node_count * nf / dt,

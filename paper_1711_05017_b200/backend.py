@@ -230,6 +230,11 @@ class HapticServer:
         check(LIB.gf_server_start(self.W1.handle, self.W2.handle, int(self.wrap), dptr(self.dom), self.dcell,
                                   dptr(self.center), self.bits, float(idle_timeout_s), ctypes.byref(sid)))
         self.id = sid.value
+        # one throw-away query: returns once the resident grid is up and its
+        # code and windows are warm, so the first real frame pays neither
+        R0, z = np.eye(3) if d == 3 else np.eye(2), np.zeros(d)
+        warm = np.zeros(14)
+        check(LIB.gf_server_query(self.id, dptr(np.ascontiguousarray(R0)), dptr(z), dptr(warm)))
         self.key = (self.W1.handle, self.W2.handle, self.wrap, self.bits)
         cd = np.zeros(6)  # center (3) | domega (3), as laid out in the query buffer
         cd[:d], cd[3:3 + d] = self.center, self.dom

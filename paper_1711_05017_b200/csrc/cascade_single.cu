@@ -161,7 +161,6 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     int ia = tid / 3, ib = tid % 3;
     sp.mu[ia][ib] = -src[ib * 3 + ia] * a.rdom[ib][ia];
   }
-  if (tid >= 16 && tid < 19) sp.targ[tid - 16] = a.dom[tid - 16] * src[9 + tid - 16];
   if (tid >= 32 && tid < 32 + 27) {  // A_g = Omega_g R (_core.pyx:615-626)
     const int k = tid - 32, g = k / 9, bb = (k / 3) % 3, ax = k % 3;
     const double* Rr = src;  // row-major R
@@ -190,27 +189,27 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     sp.ufix[ia][ib] = ib == 3 ? to_fix32((double)(ia == 0 ? hx : (ia == 1 ? hy : hz)))
                               : to_fix32(-src[ib * 3 + ia] * a.rdom[ib][ia]);
   }
-  __syncthreads();
-  if (tid == 0) {
+  if (tid == 160) {  // lane order for this pose (warp 5, from the pose itself: no barrier before it)
+    const double z0 = fabs(src[2] * a.rdom[0][2]), z1 = fabs(src[5] * a.rdom[1][2]),
+                 z2 = fabs(src[8] * a.rdom[2][2]);  // |mu[2][b]|
     int r = 2;
-    if (a.dim == 3) {
-      double z0 = fabs(sp.mu[2][0]), z1 = fabs(sp.mu[2][1]), z2 = fabs(sp.mu[2][2]);
-      r = (z0 <= z1 && z0 <= z2) ? 0 : (z1 <= z2 ? 1 : 2);
-    }
+    if (a.dim == 3) r = (z0 <= z1 && z0 <= z2) ? 0 : (z1 <= z2 ? 1 : 2);
     int o1 = (r + 1) % 3, o2 = (r + 2) % 3;
     if (a.dim == 2) { o1 = 0; o2 = 1; }
-    bool sw = fabs(sp.mu[2][o1]) > fabs(sp.mu[2][o2]);
+    const double zo1 = o1 == 0 ? z0 : (o1 == 1 ? z1 : z2), zo2 = o2 == 0 ? z0 : (o2 == 1 ? z1 : z2);
+    bool sw = zo1 > zo2;
     sp.p = sw ? o2 : o1;
     sp.q = sw ? o1 : o2;
     sp.r = r;
     sp.nP = ((sp.p == 0 ? w0 : (sp.p == 1 ? w1 : w2)) + 15) / 16;
     sp.nQ = ((sp.q == 0 ? w0 : (sp.q == 1 ? w1 : w2)) + 15) / 16;
   }
+  // per-axis translation phase tables, concurrently with the sections above
   for (int i = tid; i < w0 + w1 + w2; i += kThreads) {
     int ax = i < w0 ? 0 : (i < w0 + w1 ? 1 : 2);
     int k = i - (ax == 0 ? 0 : (ax == 1 ? w0 : w0 + w1));
     int hh = ax == 0 ? hx : (ax == 1 ? hy : hz);
-    double cyc = sp.targ[ax] * (double)(k - hh);
+    double cyc = (a.dom[ax] * src[9 + ax]) * (double)(k - hh);
     cyc -= rint(cyc);
     T sn, cs;
     if constexpr (sizeof(T) == 4) sincospif(2.0f * (float)cyc, &sn, &cs);

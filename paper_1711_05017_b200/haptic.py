@@ -13,7 +13,9 @@ in 3D and on the GPU:
   cascade launch and the first trial (in the reference's order) whose energy
   does not exceed the current one is taken -- the same decision, one launch.
 * `run` paces a trajectory at a fixed servo rate (the paper's 1 kHz loop,
-  PAPER.md:317-321) and records per-frame latency and deadline misses.
+  PAPER.md:317-321) and records per-frame latency and deadline misses; by
+  default the frames are served by a resident query grid (no launch per
+  frame).
 """
 
 from __future__ import annotations
@@ -79,8 +81,20 @@ class HapticSession:
                 return True
         return False  # every trial climbed: hold the pose
 
-    def run(self, rotations, translations, rate_hz=1000.0):
-        """Pace a pose trajectory at `rate_hz`; returns latency stats and misses."""
+    def run(self, rotations, translations, rate_hz=1000.0, resident=True):
+        """Pace a pose trajectory at `rate_hz`; returns latency stats and misses.
+
+        resident=True serves the frames from a persistent query grid
+        (energy.haptic_session) for the duration of the run, as a dedicated
+        haptic server would; False launches one kernel per frame."""
+        if resident:
+            from .energy import haptic_session
+
+            with haptic_session(self.fixed, self.moving, self.modes):
+                return self._run(rotations, translations, rate_hz)
+        return self._run(rotations, translations, rate_hz)
+
+    def _run(self, rotations, translations, rate_hz):
         period = 1.0 / rate_hz
         lat, misses = [], 0
         t_next = time.perf_counter()
