@@ -411,3 +411,102 @@ def cascade_term_scales(C1, C2, wrap, domega, dcell, R, t_eff, center):
         t2 = 2j * np.pi * (W @ (G @ (R @ center))) * V
         out.append(np.sum(np.abs(base * t1)) + np.sum(np.abs(base * t2)))
     return dcell * np.asarray(out)
+
+
+# ---------------------------------------------------------------------------
+# Independent real-space / direct-sum references for the query and landscape
+# (restating the reference's slow paths, /root/reference/pkg/src/geofield/
+# oracle.py:30-136 and :224-275, in this package's own terms).
+
+
+def node_interp(values, dims, origin, spacing, Q, wrap):
+    """Multilinear interpolation of node values at physical points Q (m, d):
+    zero outside the node box, or periodic when wrap (oracle.py:30-57)."""
+    dims = tuple(dims)
+    d = len(dims)
+    vals = np.asarray(values).reshape(dims)
+    u = (np.asarray(Q, dtype=np.float64) - np.asarray(origin, dtype=np.float64)) / spacing
+    i0 = np.floor(u).astype(np.int64)
+    fr = u - i0
+    acc = np.zeros(len(u), dtype=np.complex128)
+    for corner in np.ndindex(*(2,) * d):
+        idx = i0 + np.asarray(corner)
+        wgt = np.prod(np.where(np.asarray(corner) == 1, fr, 1.0 - fr), axis=1)
+        if wrap:
+            acc += wgt * vals[tuple((idx % np.asarray(dims)).T)]
+        else:
+            inside = np.all((idx >= 0) & (idx < np.asarray(dims)), axis=1)
+            safe = np.where(inside[:, None], idx, 0)
+            acc += np.where(inside, wgt * vals[tuple(safe.T)], 0.0)
+    return acc
+
+
+def brute_score(v1, v2, dims, origin, spacing, R, t, wrap=False):
+    """sum_j rho1(p_j) rho2(R^T (p_j - t)) dV over the grid nodes
+    (oracle.py:60-74)."""
+    P = grid_points(dims, origin, spacing)
+    Q = (P - np.asarray(t, dtype=np.float64)) @ np.asarray(R, dtype=np.float64)
+    s = node_interp(v2, dims, origin, spacing, Q, wrap)
+    return complex(np.sum(np.asarray(v1).ravel() * s) * spacing ** len(dims))
+
+
+def direct_amplitudes(values, dims, origin, spacing, W):
+    """A(w) = sum_i f_i exp(-2 pi i w.p_i) dV at arbitrary frequencies W (k, d)
+    by explicit summation (oracle.py:85-93)."""
+    P = grid_points(dims, origin, spacing)
+    f = np.asarray(values).ravel()
+    dV = spacing ** len(dims)
+    return np.array([np.sum(f * np.exp(-2j * np.pi * (P @ w))) * dV for w in np.asarray(W)])
+
+
+def cascade_direct(v1, v2, dims, origin, spacing, R, t, side=None):
+    """Mode sum with exactly rotated amplitudes (no interpolation): the
+    band-limited score over the centred window of `side` modes per axis
+    (oracle.py:105-136)."""
+    dims = tuple(dims)
+    d = len(dims)
+    dom = np.array([1.0 / (n * spacing) for n in dims])
+    sides = dims if side is None else (side,) * d
+    W = window_freqs(sides, dom)
+    A1 = direct_amplitudes(v1, dims, origin, spacing, W)
+    A2 = direct_amplitudes(v2, dims, origin, spacing, -(W @ np.asarray(R, dtype=np.float64)))
+    dcell = 1.0 / (np.prod(dims) * spacing ** d)
+    return complex(np.sum(A1 * A2 * np.exp(2j * np.pi * (W @ np.asarray(t, dtype=np.float64)))) * dcell)
+
+
+def axis_rotation(d, axis, angle):
+    if d == 2:
+        c, s = np.cos(angle), np.sin(angle)
+        return np.array([[c, -s], [s, c]])
+    k = np.zeros(3)
+    k[axis] = 1.0
+    K = np.array([[0, -k[2], k[1]], [k[2], 0, -k[0]], [-k[1], k[0], 0]])
+    return np.eye(3) + np.sin(angle) * K + (1 - np.cos(angle)) * (K @ K)
+
+
+def fd_gradient(scorer, R, t, dt=1e-6, dr=1e-6):
+    """Central differences of scorer(R, t): translation components, then the
+    left-multiplied rotation generators, with the rotation step refined until
+    two estimates agree (oracle.py:234-275)."""
+    R = np.asarray(R, dtype=np.float64)
+    t = np.asarray(t, dtype=np.float64)
+    d = len(t)
+    tg = np.empty(d, dtype=np.complex128)
+    for a in range(d):
+        e = np.zeros(d)
+        e[a] = dt
+        tg[a] = (scorer(R, t + e) - scorer(R, t - e)) / (2 * dt)
+    n_rot = 1 if d == 2 else 3
+    rg = np.empty(n_rot, dtype=np.complex128)
+    for g in range(n_rot):
+        step = dr
+        est = (scorer(axis_rotation(d, g, step) @ R, t) - scorer(axis_rotation(d, g, -step) @ R, t)) / (2 * step)
+        for _ in range(3):
+            step /= 10.0
+            finer = (scorer(axis_rotation(d, g, step) @ R, t) - scorer(axis_rotation(d, g, -step) @ R, t)) / (2 * step)
+            done = abs(finer - est) <= 1e-4 * max(abs(finer), 1e-12)
+            est = finer
+            if done:
+                break
+        rg[g] = est
+    return tg, rg

@@ -6,6 +6,8 @@ import numpy as np, torch
 from paper_1711_05017_b200 import backend as be, _lib
 from conftest import synthetic_window, random_rotation
 _lib.ensure_device(0)
+if os.environ.get('GF_TILE'):
+    _lib.check(_lib.LIB.gf_set_cascade_tile(int(os.environ['GF_TILE'])))
 rng = np.random.default_rng(0)
 w = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 W1, W2 = be.DeviceWindow(synthetic_window(rng, w)), be.DeviceWindow(synthetic_window(rng, w))
