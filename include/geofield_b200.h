@@ -105,7 +105,9 @@ int gf_sweep(int d, const double *elems, const double *normals, const double *me
  * InverseSquare, values = winding), combine, neighbour fill of excluded
  * nodes.  values_dev: complex128 node values (device); flags_dev: one byte
  * per node (bit0 excluded, bit1 unresolved, bit2 inside); stats[0] = total
- * eta clamps, stats[1] = worst residual. */
+ * eta clamps, stats[1] = worst residual, stats[2] = seconds of the fused
+ * distance + winding kernel, stats[3] = seconds of the sweep (device time);
+ * `stats` holds 4 doubles. */
 int gf_affinity_grid(int d, const double *elems, const double *normals, const double *measures, int64_t ne,
                      const int32_t *dims, const double *origin, double spacing, int family, double sigma,
                      double gconst, double lam_in, double lam_out, double max_angle, int max_depth, double eta_floor,

@@ -510,3 +510,25 @@ def fd_gradient(scorer, R, t, dt=1e-6, dr=1e-6):
                 break
         rg[g] = est
     return tg, rg
+
+
+def disk_density(sigma, lam_in, lam_out, a, radii, n_theta=2048):
+    """Skeletal density of a disk of radius a at distance r from its centre by
+    Gauss-Legendre quadrature of the one angular boundary integral -- an
+    independent route to the swept density (oracle.py:278-318): interior
+    points take lam_in * conj(I), exterior -lam_out * I."""
+    x, wts = np.polynomial.legendre.leggauss(n_theta)
+    th = np.pi * (x + 1.0)
+    wq = np.pi * wts
+    qx, qy = a * np.cos(th), a * np.sin(th)
+    out = []
+    for r in np.atleast_1d(radii):
+        xi = abs(r - a)
+        rx, ry = qx - r, qy
+        eta = np.hypot(rx, ry)
+        proj = (qx * rx + qy * ry) / (a * eta)
+        g = np.exp(-0.5 * ((eta / xi - 1.0) / sigma) ** 2) / (np.sqrt(2.0 * np.pi) * sigma)
+        z = xi + 1j * eta
+        I = np.sum(wq * g * proj / (z * z)) * a / (2.0 * np.pi)
+        out.append(lam_in * np.conj(I) if r < a else -lam_out * I)
+    return np.asarray(out)

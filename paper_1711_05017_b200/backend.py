@@ -362,7 +362,7 @@ def affinity_grid(solid, grid, family, sigma, gconst, lam_in, lam_out, max_angle
 
     Returns (values: CUDA complex128 tensor of grid.node_count, flags: CUDA
     uint8 tensor (bit0 excluded, bit1 unresolved, bit2 inside), stats
-    (total clamps, worst residual))."""
+    (total clamps, worst residual, distance+winding seconds, sweep seconds))."""
     import torch
 
     dev = _lib.ensure_device()
@@ -370,7 +370,7 @@ def affinity_grid(solid, grid, family, sigma, gconst, lam_in, lam_out, max_angle
     m = grid.node_count
     values = torch.empty(m, dtype=torch.complex128, device=f"cuda:{dev}")
     flags = torch.empty(m, dtype=torch.uint8, device=f"cuda:{dev}")
-    stats = np.zeros(2)
+    stats = np.zeros(4)
     dims = (ctypes.c_int32 * 3)(*(list(grid.dims) + [1] * (3 - len(grid.dims))))
     origin = np.zeros(3)
     origin[:grid.dimension] = grid.origin
@@ -380,7 +380,7 @@ def affinity_grid(solid, grid, family, sigma, gconst, lam_in, lam_out, max_angle
                                float(gconst), float(lam_in), float(lam_out), float(max_angle), int(max_depth),
                                float(eta_floor), ctypes.c_void_p(values.data_ptr()),
                                ctypes.c_void_p(flags.data_ptr()), dptr(stats), ctypes.c_void_p(st)))
-    return values, flags, (int(stats[0]), float(stats[1]))
+    return values, flags, (int(stats[0]), float(stats[1]), float(stats[2]), float(stats[3]))
 
 
 def affinity_planes(solid, grid, plane0, nplanes, halo_lo, halo_hi, family, sigma, gconst, lam_in, lam_out, max_angle,
@@ -396,7 +396,7 @@ def affinity_planes(solid, grid, plane0, nplanes, halo_lo, halo_hi, family, sigm
     m = int(nplanes) * plane
     values = torch.empty(m, dtype=torch.complex128, device=f"cuda:{dev}")
     flags = torch.empty(m, dtype=torch.uint8, device=f"cuda:{dev}")
-    stats = np.zeros(2)
+    stats = np.zeros(4)
     dims = (ctypes.c_int32 * 3)(*(list(grid.dims) + [1] * (3 - len(grid.dims))))
     origin = np.zeros(3)
     origin[:grid.dimension] = grid.origin
@@ -407,4 +407,4 @@ def affinity_planes(solid, grid, plane0, nplanes, halo_lo, halo_hi, family, sigm
                                  float(lam_out), float(max_angle), int(max_depth), float(eta_floor),
                                  ctypes.c_void_p(values.data_ptr()), ctypes.c_void_p(flags.data_ptr()), dptr(stats),
                                  ctypes.c_void_p(st)))
-    return values, flags, (int(stats[0]), float(stats[1]))
+    return values, flags, (int(stats[0]), float(stats[1]), float(stats[2]), float(stats[3]))

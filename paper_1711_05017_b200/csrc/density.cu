@@ -586,11 +586,22 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
   src.spacing = spacing;
   const double eta_min = eta_floor * spacing;
   unsigned grid = (unsigned)ceil_div(m, kThreads);
+  // per-stage device time for the stats (the reference reports seconds_*)
+  cudaEvent_t ev[3];
+  for (auto& e : ev) GF_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 3; ++i) cudaEventDestroy(e[i]);
+    }
+  } ev_guard{ev};
+  GF_CUDA(cudaEventRecord(ev[0], st));
   if (d == 3)
     dist_wind_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dxi.p, (double*)dwind.p);
   else
     dist_wind_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dxi.p, (double*)dwind.p);
   GF_CUDA(cudaGetLastError());
+  GF_CUDA(cudaEventRecord(ev[1], st));
   if (family != 0) {
     // xi_eff = max(xi, eta_min) (descriptor.py:338)
     GF_CUDA(cudaMalloc(&dxe.p, sizeof(double) * m));
@@ -607,6 +618,7 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
                                                  (int64_t*)dcl.p);
     GF_CUDA(cudaGetLastError());
   }
+  GF_CUDA(cudaEventRecord(ev[2], st));
   combine_kernel<<<148 * 8, 256, 0, st>>>(m, (const double*)dxi.p, (const double*)dwind.p, (const double*)dip.p,
                                           (const double*)dres.p, family, lam_in, lam_out, eta_min, max_angle,
                                           (double*)dval.p, out_flags);
@@ -630,6 +642,11 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
   GF_CUDA(cudaStreamSynchronize(st));
   stats[0] = (double)hs[0];
   stats[1] = __longlong_as_double_host(hs[1]);
+  float ms_dw = 0.f, ms_sw = 0.f;
+  GF_CUDA(cudaEventElapsedTime(&ms_dw, ev[0], ev[1]));
+  GF_CUDA(cudaEventElapsedTime(&ms_sw, ev[1], ev[2]));
+  stats[2] = 1e-3 * ms_dw;
+  stats[3] = 1e-3 * ms_sw;
   return 0;
 }
 

@@ -253,7 +253,8 @@ def affinity_field_slab(solid, grid, spec, policy=None, group=None, gather=True,
                                            _unit_constant(grid.dimension), spec.lambda_in, spec.lambda_out,
                                            policy.max_solid_angle, policy.max_recursion_depth, policy.eta_floor)
     if n > 0:
-        values, fb, (nclamp, worst) = compute(solid, grid, plane0, n, hlo, hhi)
+        values, fb, st = compute(solid, grid, plane0, n, hlo, hhi)
+        nclamp, worst = st[0], st[1]
     else:
         values = torch.empty(0, dtype=torch.complex128)
         fb = torch.empty(0, dtype=torch.uint8)

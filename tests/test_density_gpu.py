@@ -116,11 +116,11 @@ def test_node_slabs_bit_identical_to_whole_grid(scene, n):
     pol = IntegrationPolicy()
     args = (1, KERNEL.sigma, _unit_constant(g.dimension), KERNEL.lambda_in, KERNEL.lambda_out, pol.max_solid_angle,
             pol.max_recursion_depth, pol.eta_floor)
-    v0, f0, (c0, w0) = backend.affinity_grid(sc.fixed, g, *args)
+    v0, f0, (c0, w0, _, _) = backend.affinity_grid(sc.fixed, g, *args)
     for world in (2, 3, 5):
         vs, fs, cl, wr = [], [], 0, 0.0
         for p0, k, lo, hi in parallel.density_slab_plan(g.dims[0], world):
-            v, f, (c, w) = backend.affinity_planes(sc.fixed, g, p0, k, lo, hi, *args)
+            v, f, (c, w, _, _) = backend.affinity_planes(sc.fixed, g, p0, k, lo, hi, *args)
             vs.append(v)
             fs.append(f)
             cl += c
