@@ -532,3 +532,42 @@ def disk_density(sigma, lam_in, lam_out, a, radii, n_theta=2048):
         I = np.sum(wq * g * proj / (z * z)) * a / (2.0 * np.pi)
         out.append(lam_in * np.conj(I) if r < a else -lam_out * I)
     return np.asarray(out)
+
+
+def raycast_inside(triangles, P, seed=0):
+    """Point-in-mesh by ray-crossing parity (an independent test of the
+    winding classification; reference oracle.py:161-221): one random
+    direction per batch, Moller-Trumbore hits, and points whose ray grazes an
+    edge or vertex (barycentric within 1e-9 of the boundary) are re-cast with
+    a fresh direction."""
+    tri = np.asarray(triangles, dtype=np.float64).reshape(-1, 3, 3)
+    P = np.asarray(P, dtype=np.float64)
+    rng = np.random.default_rng(seed)
+    out = np.zeros(len(P), dtype=bool)
+    todo = np.arange(len(P))
+    a, e1, e2 = tri[:, 0], tri[:, 1] - tri[:, 0], tri[:, 2] - tri[:, 0]
+    while len(todo):
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        pv = np.cross(d, e2)                      # (n, 3)
+        det = np.einsum("ij,ij->i", e1, pv)
+        ok_det = np.abs(det) > 1e-14
+        inv = np.where(ok_det, 1.0 / np.where(ok_det, det, 1.0), 0.0)
+        graze = np.zeros(len(todo), dtype=bool)
+        count = np.zeros(len(todo), dtype=np.int64)
+        for c0 in range(0, len(todo), 512):
+            idx = todo[c0:c0 + 512]
+            s = P[idx][:, None, :] - a[None, :, :]   # (m, n, 3)
+            u = np.einsum("mnk,nk->mn", s, pv) * inv
+            q = np.cross(s, e1[None, :, :])
+            v = np.einsum("k,mnk->mn", d, q) * inv
+            t = np.einsum("nk,mnk->mn", e2, q) * inv
+            hit = ok_det & (u >= 0) & (v >= 0) & (u + v <= 1) & (t > 0)
+            near = ok_det & (t > 0) & ((np.abs(u) < 1e-9) | (np.abs(v) < 1e-9) | (np.abs(u + v - 1) < 1e-9)) & \
+                (u > -1e-9) & (v > -1e-9) & (u + v < 1 + 1e-9)
+            count[c0:c0 + 512] = hit.sum(axis=1)
+            graze[c0:c0 + 512] = near.any(axis=1)
+        done = ~graze
+        out[todo[done]] = (count[done] % 2) == 1
+        todo = todo[graze]
+    return out
