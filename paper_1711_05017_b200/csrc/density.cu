@@ -24,6 +24,8 @@
 #include "common.cuh"
 
 #include <math.h>
+
+#include <map>
 #include <string.h>
 
 namespace gf {
@@ -441,14 +443,49 @@ double __longlong_as_double_host(unsigned long long b) {
   return d;
 }
 
+// Per-thread cache of device blocks for the per-call buffers: repeated
+// fields of the same size reuse memory instead of paying cudaMalloc and the
+// device-synchronising cudaFree every call.  Blocks go back to the cache
+// when the entry point returns (after its final stream synchronisation).
+struct BlockCache {
+  std::multimap<size_t, void*> free_blocks;
+  size_t cached = 0;
+  ~BlockCache() {
+    for (auto& kv : free_blocks) cudaFree(kv.second);  // process exit: errors ignored
+  }
+};
+thread_local BlockCache tl_blocks;
+constexpr size_t kBlockCacheCap = size_t(8) << 30;
+
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() { gf::device_free(p); }
+  size_t n = 0;
+  cudaError_t alloc(size_t bytes) {
+    auto it = tl_blocks.free_blocks.lower_bound(bytes);
+    if (it != tl_blocks.free_blocks.end() && it->first <= 2 * bytes + (1 << 20)) {
+      p = it->second;
+      n = it->first;
+      tl_blocks.cached -= n;
+      tl_blocks.free_blocks.erase(it);
+      return cudaSuccess;
+    }
+    n = bytes;
+    return cudaMalloc(&p, bytes);
+  }
+  ~DevBuf() {
+    if (!p) return;
+    if (tl_blocks.cached + n > kBlockCacheCap) {
+      gf::device_free(p);
+      return;
+    }
+    tl_blocks.free_blocks.emplace(n, p);
+    tl_blocks.cached += n;
+  }
 };
 
 int upload(const void* host, size_t bytes, DevBuf& b, cudaStream_t st) {
   if (bytes == 0) return 0;
-  GF_CUDA(cudaMalloc(&b.p, bytes));
+  GF_CUDA(b.alloc(bytes));
   GF_CUDA(cudaMemcpyAsync(b.p, host, bytes, cudaMemcpyHostToDevice, st));
   return 0;
 }
@@ -473,8 +510,8 @@ int gf_distance_winding(int d, const double* elems, int64_t ne, const double* P,
   const int E = d == 3 ? 9 : 4;
   if ((rc = upload(elems, sizeof(double) * E * ne, de, st))) return rc;
   if ((rc = upload(P, sizeof(double) * d * m, dp, st))) return rc;
-  if (xi_out) GF_CUDA(cudaMalloc(&dx.p, sizeof(double) * m));
-  if (wind_out) GF_CUDA(cudaMalloc(&dw.p, sizeof(double) * m));
+  if (xi_out) GF_CUDA(dx.alloc(sizeof(double) * m));
+  if (wind_out) GF_CUDA(dw.alloc(sizeof(double) * m));
   PointSource src = {};
   src.P = (const double*)dp.p;
   src.d = d;
@@ -509,7 +546,7 @@ int gf_sweep(int d, const double* elems, const double* normals, const double* me
   if ((rc = upload(xi_eff, sizeof(double) * m, dx, st))) return rc;
   if ((rc = upload(resid, sizeof(double) * m, dres, st))) return rc;
   if ((rc = upload(clamps, sizeof(int64_t) * m, dcl, st))) return rc;
-  GF_CUDA(cudaMalloc(&dout.p, sizeof(double) * 2 * m));
+  GF_CUDA(dout.alloc(sizeof(double) * 2 * m));
   PointSource src = {};
   src.P = (const double*)dp.p;
   src.d = d;
@@ -557,20 +594,20 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
   if ((rc = upload(elems, sizeof(double) * E * ne, de, st))) return rc;
   if ((rc = upload(normals, sizeof(double) * d * ne, dn, st))) return rc;
   if ((rc = upload(measures, sizeof(double) * ne, dm, st))) return rc;
-  GF_CUDA(cudaMalloc(&dxi.p, sizeof(double) * m));
-  GF_CUDA(cudaMalloc(&dwind.p, sizeof(double) * m));
-  GF_CUDA(cudaMalloc(&dres.p, sizeof(double) * m));
-  GF_CUDA(cudaMalloc(&dcl.p, sizeof(int64_t) * m));
-  GF_CUDA(cudaMalloc(&dip.p, sizeof(double) * 2 * m));
-  GF_CUDA(cudaMalloc(&dval.p, sizeof(double) * 2 * m));
+  GF_CUDA(dxi.alloc(sizeof(double) * m));
+  GF_CUDA(dwind.alloc(sizeof(double) * m));
+  GF_CUDA(dres.alloc(sizeof(double) * m));
+  GF_CUDA(dcl.alloc(sizeof(int64_t) * m));
+  GF_CUDA(dip.alloc(sizeof(double) * 2 * m));
+  GF_CUDA(dval.alloc(sizeof(double) * 2 * m));
   GF_CUDA(cudaMemsetAsync(dres.p, 0, sizeof(double) * m, st));
   GF_CUDA(cudaMemsetAsync(dcl.p, 0, sizeof(int64_t) * m, st));
   // with halo planes, fill a full computed block and hand back the owned part
   void* out_vals = values_dev;
   uint8_t* out_flags = flags_dev;
   if (halos) {
-    GF_CUDA(cudaMalloc(&hval.p, sizeof(double) * 2 * m));
-    GF_CUDA(cudaMalloc(&hflg.p, m));
+    GF_CUDA(hval.alloc(sizeof(double) * 2 * m));
+    GF_CUDA(hflg.alloc(m));
     out_vals = hval.p;
     out_flags = (uint8_t*)hflg.p;
   }
@@ -604,7 +641,7 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
   GF_CUDA(cudaEventRecord(ev[1], st));
   if (family != 0) {
     // xi_eff = max(xi, eta_min) (descriptor.py:338)
-    GF_CUDA(cudaMalloc(&dxe.p, sizeof(double) * m));
+    GF_CUDA(dxe.alloc(sizeof(double) * m));
     clamp_min_kernel<<<148 * 8, 256, 0, st>>>((const double*)dxi.p, (double*)dxe.p, m, eta_min);
     GF_CUDA(cudaGetLastError());
     SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
@@ -632,7 +669,7 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     GF_CUDA(cudaMemcpyAsync(flags_dev, out_flags + off, own, cudaMemcpyDeviceToDevice, st));
   }
   DevBuf dst;
-  GF_CUDA(cudaMalloc(&dst.p, 2 * sizeof(unsigned long long)));
+  GF_CUDA(dst.alloc(2 * sizeof(unsigned long long)));
   GF_CUDA(cudaMemsetAsync(dst.p, 0, 2 * sizeof(unsigned long long), st));
   stats_kernel<<<148 * 4, 256, 0, st>>>((const double*)dres.p + off, (const int64_t*)dcl.p + off, own,
                                         (unsigned long long*)dst.p);

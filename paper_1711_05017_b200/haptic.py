@@ -95,7 +95,18 @@ class HapticSession:
         return self._run(rotations, translations, rate_hz)
 
     def _run(self, rotations, translations, rate_hz):
+        import gc
+
         period = 1.0 / rate_hz
+        gc_was = gc.isenabled()
+        gc.disable()  # a collector pause inside the servo loop would be a missed frame
+        try:
+            return self._paced(rotations, translations, period, rate_hz)
+        finally:
+            if gc_was:
+                gc.enable()
+
+    def _paced(self, rotations, translations, period, rate_hz):
         lat, misses = [], 0
         t_next = time.perf_counter()
         for R, t in zip(rotations, translations):
