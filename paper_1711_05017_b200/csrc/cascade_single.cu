@@ -218,9 +218,6 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   }
   __syncthreads();
 
-  const cx<T>* px = ptab;
-  const cx<T>* py = ptab + w0;
-  const cx<T>* pz = ptab + w0 + w1;
   const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
   const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
   const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
@@ -247,27 +244,55 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   const int u_begin = a.tile == 0 ? blockIdx.x * upb : blockIdx.x;
   const int u_step = a.tile == 0 ? 1 : gridDim.x;
   const int u_end = a.tile == 0 ? min(units, u_begin + upb) : units;
+  // Along a CTA's contiguous unit range consecutive units are consecutive
+  // run-axis planes of one (p, q) patch: the fixed-point index advances by
+  // one exact integer add per axis and the p/q phase product is reused.
+  const cx<T>* pt_p = ptab + (p == 0 ? 0 : (p == 1 ? w0 : w0 + w1));
+  const cx<T>* pt_q = ptab + (q == 0 ? 0 : (q == 1 ? w0 : w0 + w1));
+  const cx<T>* pt_r = ptab + (r == 0 ? 0 : (r == 1 ? w0 : w0 + w1));
+  long long fxr = 0, fyr = 0, fzr = 0;  // d(u_a)/d(k_r) in 32.32 fixed point
+  if constexpr (sizeof(T) == 4) {
+    fxr = r == 0 ? sp.ufix[0][0] : (r == 1 ? sp.ufix[0][1] : sp.ufix[0][2]);
+    fyr = r == 0 ? sp.ufix[1][0] : (r == 1 ? sp.ufix[1][1] : sp.ufix[1][2]);
+    fzr = r == 0 ? sp.ufix[2][0] : (r == 1 ? sp.ufix[2][1] : sp.ufix[2][2]);
+  }
+  long long fu3[3] = {0, 0, 0};
+  cx<T> ph_pq = mk<T>(1, 0);
+  int prev_run = -1, prev_kr = -2;
   for (int unit = u_begin; unit < u_end; unit += u_step) {
     const int kr = unit % wr;
-    const int iq = (unit / wr) % sp.nQ;
-    const int ip = unit / (wr * sp.nQ);
+    const int run = unit / wr;
+    const int iq = run % sp.nQ;
+    const int ip = run / sp.nQ;
     const int kp = 16 * ip + dp, kq = 16 * iq + dq;
     if (kp >= wp || kq >= wq) continue;
     const int kx = p == 0 ? kp : (q == 0 ? kq : kr);
     const int ky = p == 1 ? kp : (q == 1 ? kq : kr);
     const int kz = p == 2 ? kp : (q == 2 ? kq : kr);
     const T kapx = (T)(kx - hx), kapy = (T)(ky - hy), kapz = (T)(kz - hz);
+    const bool step = run == prev_run && kr == prev_kr + 1;
+    if (!step) ph_pq = pt_p[kp] * pt_q[kq];
+    prev_run = run;
+    prev_kr = kr;
     T fl[3], f[3];
     if constexpr (sizeof(T) == 4) {
       // exact 32.32 fixed-point index; float64 reference order only within 1e-6 of an integer
+      if (step) {
+        fu3[0] += fxr;
+        fu3[1] += fyr;
+        fu3[2] += fzr;
+      } else {
+        const int kk[3] = {kx - hx, ky - hy, kz - hz};
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+          fu3[ax] = sp.ufix[ax][3] + (long long)kk[0] * sp.ufix[ax][0] + (long long)kk[1] * sp.ufix[ax][1] +
+                    (long long)kk[2] * sp.ufix[ax][2];
+      }
       unsigned lo[3];
-      const int kk[3] = {kx - hx, ky - hy, kz - hz};
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
-        const long long u = sp.ufix[ax][3] + (long long)kk[0] * sp.ufix[ax][0] + (long long)kk[1] * sp.ufix[ax][1] +
-                            (long long)kk[2] * sp.ufix[ax][2];
-        lo[ax] = fix_lo(u);
-        fl[ax] = (T)fix_floor(u);
+        lo[ax] = fix_lo(fu3[ax]);
+        fl[ax] = (T)fix_floor(fu3[ax]);
         f[ax] = fix_frac(lo[ax]);
       }
       const bool tz = a.dim == 3 && fix_tie(lo[2]);
@@ -315,7 +340,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     }
     const P4* ptr = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
     P4 e00 = ldg_pair(ptr), e10 = ldg_pair(ptr + sx), e01 = ldg_pair(ptr + sy), e11 = ldg_pair(ptr + sx + sy);
-    const cx<T> base = C1[(kx * w1 + ky) * w2 + kz] * ((px[kx] * py[ky]) * pz[kz]);
+    const cx<T> base = C1[(kx * w1 + ky) * w2 + kz] * (ph_pq * pt_r[kr]);
     const T fu = f[0], fv = f[1], fs = f[2];
     cx<T> c000 = mk<T>(e00.x, e00.y), c001 = mk<T>(e00.z, e00.w);
     cx<T> c100 = mk<T>(e10.x, e10.y), c101 = mk<T>(e10.z, e10.w);
