@@ -531,6 +531,109 @@ __global__ void __launch_bounds__(B / 2 * (N / 8), 2) fft_pair_kernel(FftArgs a)
   }
 }
 
+// Strided y pass fused with the slab exchange of the multi-GPU landscape
+// (parallel.score_field_slab): the transformed lines are stored straight into
+// the destination rank's y-slab -- a peer GPU's buffer over NVLink when the
+// pointer is a peer mapping -- instead of a local buffer followed by an
+// all-to-all.  Element (x, y, z) of this rank's planes lands in rank s with
+// ybound[s] <= y < ybound[s+1] at ((x_off + x) * ny_s + y - ybound[s]) * N2 + z.
+// Loads, butterflies and scaling are those of fft_kernel (bitwise the same
+// values); lanes walk 16 (8) adjacent z, so every store is a 128-byte row.
+constexpr int kMaxScatter = 8;
+struct ScatterOut {
+  int nranks;
+  int ybound[kMaxScatter + 1];
+  void* dst[kMaxScatter];
+  int x_off;
+};
+
+template <typename T, int N, int B>
+__global__ void __launch_bounds__(B * (N / 8)) fft_scatter_kernel(FftArgs a, ScatterOut so) {
+  constexpr int TPL = N / 8;
+  constexpr int LD = LineLD<T, N>::value;
+  extern __shared__ __align__(128) unsigned char fft_smem[];
+  cx<T>* buf = reinterpret_cast<cx<T>*>(fft_smem);
+  const int tid = threadIdx.x;
+  const int b = tid % B, j = tid / B;
+  const int Lin = a.shape_in[1], s2 = a.shape_in[2];
+  const int ptiles = (s2 + B - 1) / B;
+  const int o = blockIdx.x / ptiles, p = (blockIdx.x % ptiles) * B + b;
+  const bool live = p < s2;
+  const cx<T>* __restrict__ in = reinterpret_cast<const cx<T>*>(a.in);
+  const cx<T>* __restrict__ tw = reinterpret_cast<const cx<T>*>(a.tw);
+  const int64_t base_in = (int64_t)o * Lin * s2 + p;
+  const int hin = Lin / 2;
+  cx<T> v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int pos = j + r * TPL;
+    int src, m;
+    if (a.in_centered) {
+      m = pos < N / 2 ? pos : pos - N;
+      src = m + hin;
+      if (src < 0 || src >= Lin) src = -1;
+    } else {
+      m = pos;
+      src = pos;
+    }
+    cx<T> x = mk<T>(0, 0);
+    if (live && src >= 0) {
+      x = in[base_in + (int64_t)src * s2];
+      if (a.in_phase_kind) x = x * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
+    }
+    v[r] = x;
+  }
+  cx<T>* line = buf + b * LD;
+  fft_line<T, N>(v, line, j, tw, a.sign);
+  if (!live) return;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int y = j + r * TPL;  // node order
+    int s = 0;
+    while (s + 1 < so.nranks && y >= so.ybound[s + 1]) ++s;
+    const int ny = so.ybound[s + 1] - so.ybound[s];
+    cx<T> val = line[sidx<T>(y)];
+    val = mk<T>(val.re * (T)a.scale, val.im * (T)a.scale);
+    cx<T>* dst = reinterpret_cast<cx<T>*>(so.dst[s]);
+    dst[((int64_t)(so.x_off + o) * ny + (y - so.ybound[s])) * s2 + p] = val;
+  }
+}
+
+template <typename T, int N>
+cudaError_t launch_scatter_n(const FftArgs& a, const ScatterOut& so, cudaStream_t st) {
+  constexpr int TPL = N / 8;
+  constexpr int B0 = 128 / sizeof(cx<T>);
+  constexpr int B = B0 * TPL > 1024 ? 1024 / TPL : B0;
+  constexpr size_t smem = sizeof(cx<T>) * B * LineLD<T, N>::value;
+  if (smem > 48 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(fft_scatter_kernel<T, N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+  }
+  const int64_t blocks = (int64_t)a.shape_in[0] * ceil_div(a.shape_in[2], B);
+  fft_scatter_kernel<T, N, B><<<(unsigned)blocks, B * TPL, smem, st>>>(a, so);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_scatter(const FftArgs& a, const ScatterOut& so, int n, cudaStream_t st) {
+  switch (n) {
+    case 8: return launch_scatter_n<T, 8>(a, so, st);
+    case 16: return launch_scatter_n<T, 16>(a, so, st);
+    case 32: return launch_scatter_n<T, 32>(a, so, st);
+    case 64: return launch_scatter_n<T, 64>(a, so, st);
+    case 128: return launch_scatter_n<T, 128>(a, so, st);
+    case 256: return launch_scatter_n<T, 256>(a, so, st);
+    case 512: return launch_scatter_n<T, 512>(a, so, st);
+    case 1024: return launch_scatter_n<T, 1024>(a, so, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <typename T>
 __global__ void twiddle_kernel(cx<T>* tw, int n, int sign) {
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
@@ -809,5 +912,48 @@ extern "C" int gf_fft_pass(int precision, const void* in, void* out, const int32
   a.scale = scale;
   if (precision == 64) GF_CUDA(launch_fft<double>(a, n, st));
   else GF_CUDA(launch_fft<float>(a, n, st));
+  return 0;
+}
+
+extern "C" int gf_fft_pass_scatter(int precision, const void* in, const int32_t* shape_in, int n, int in_centered,
+                                   int sign, double in_phase, double scale, int nranks, const int32_t* y_bounds,
+                                   const uint64_t* dst_ptrs, int x_off, void* stream) {
+  GF_CHECK(in && shape_in && y_bounds && dst_ptrs, GF_EINVAL, "null argument");
+  GF_CHECK(nranks >= 1 && nranks <= kMaxScatter, GF_EINVAL, "1 to 8 destination ranks");
+  GF_CHECK(n >= 8 && n <= 1024 && (n & (n - 1)) == 0, GF_EINVAL, "FFT length must be a power of two in [8, 1024]");
+  GF_CHECK(precision == 32 || precision == 64, GF_EINVAL, "precision must be 32 or 64");
+  GF_CHECK(sign == -1 || sign == 1, GF_EINVAL, "sign must be -1 or +1");
+  GF_CHECK(shape_in[1] <= n && (in_centered || shape_in[1] == n), GF_EINVAL, "bad line length");
+  GF_CHECK(y_bounds[0] == 0 && y_bounds[nranks] == n, GF_EINVAL, "y slabs must tile [0, n)");
+  for (int r = 0; r < nranks; ++r) {
+    GF_CHECK(y_bounds[r + 1] >= y_bounds[r], GF_EINVAL, "y slab bounds must be non-decreasing");
+    GF_CHECK(dst_ptrs[r] != 0 || y_bounds[r + 1] == y_bounds[r], GF_EINVAL, "null destination slab");
+  }
+  GF_CHECK(x_off >= 0, GF_EINVAL, "negative plane offset");
+  cudaStream_t st = (cudaStream_t)stream;
+  FftArgs a = {};
+  a.in = in;
+  a.out = nullptr;
+  a.tw = twiddles(precision, n, sign, st);
+  GF_CHECK(a.tw != nullptr, GF_ENOMEM, "twiddle table allocation failed");
+  for (int k = 0; k < 3; ++k) a.shape_in[k] = shape_in[k];
+  a.shape_out[0] = shape_in[0];
+  a.shape_out[1] = n;
+  a.shape_out[2] = shape_in[2];
+  a.axis = 1;
+  a.in_centered = in_centered;
+  a.out_centered = 0;
+  a.sign = sign;
+  a.in_phase = in_phase;
+  a.in_phase_kind = phase_kind(in_phase);
+  a.scale = scale;
+  ScatterOut so = {};
+  so.nranks = nranks;
+  for (int r = 0; r <= nranks; ++r) so.ybound[r] = y_bounds[r];
+  for (int r = 0; r < nranks; ++r) so.dst[r] = reinterpret_cast<void*>(dst_ptrs[r]);
+  so.x_off = x_off;
+  if (shape_in[0] == 0) return 0;
+  if (precision == 64) GF_CUDA(launch_scatter<double>(a, so, n, st));
+  else GF_CUDA(launch_scatter<float>(a, so, n, st));
   return 0;
 }

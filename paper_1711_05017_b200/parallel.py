@@ -158,10 +158,46 @@ def exchange_planes_to_slabs(local, kx_ranges, y_ranges, rank, group=None):
     return torch.cat(blocks, dim=0)
 
 
-def score_field_slab(asset1, asset2, R, m_prime=None, precision=64, group=None):
+_SYMM = {}
+
+
+def _symm_slab(shape, dtype, group):
+    """Symmetric-memory slab buffer (same size on every rank) and its
+    handle; cached per (shape, dtype, group)."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+
+    dist = _dist()
+    g = group or dist.group.WORLD
+    key = (tuple(shape), dtype, id(g))
+    if key not in _SYMM:
+        real = torch.float64 if dtype == torch.complex128 else torch.float32
+        buf = symm_mem.empty(*shape, 2, dtype=real, device=f"cuda:{_lib.ensure_device()}")
+        _SYMM[key] = (buf, symm_mem.rendezvous(buf, g))
+    return _SYMM[key]
+
+
+def scatter_y_pass(a, n1, bounds, dst_ptrs, x_off, precision):
+    """The y inverse pass of this rank's planes `a` (nk, w1, N2), stored
+    straight into the destination ranks' y-slabs (gf_fft_pass_scatter)."""
+    import torch
+
+    si = (ctypes.c_int32 * 3)(*a.shape)
+    yb = (ctypes.c_int32 * len(bounds))(*bounds)
+    dp = (ctypes.c_uint64 * len(dst_ptrs))(*dst_ptrs)
+    st = torch.cuda.current_stream(a.device).cuda_stream
+    _lib.check(_lib.LIB.gf_fft_pass_scatter(precision, ctypes.c_void_p(a.data_ptr()), si, int(n1), 1, 1, 0.0, 1.0,
+                                            len(dst_ptrs), yb, dp, int(x_off), ctypes.c_void_p(st)))
+
+
+def score_field_slab(asset1, asset2, R, m_prime=None, precision=64, group=None, exchange="auto"):
     """This rank's y-slab (N0, ny, N2) of the landscape (energy.score_field),
-    as a CUDA complex tensor; one all-to-all between the inner passes and the
-    x pass.  Gather the slabs along axis 1 for the full N^3 field."""
+    as a CUDA complex tensor.  Gather the slabs along axis 1 for the full
+    N^3 field.  The exchange between the inner passes and the x pass is
+    either fused into the y pass (exchange="fused", the default on NCCL: the
+    pass stores each line straight into its destination rank's symmetric-
+    memory slab over NVLink, then one device-side barrier) or an
+    all-to-all ("alltoall", the gloo path)."""
     import torch
 
     from .energy import _check_pair
@@ -192,10 +228,22 @@ def score_field_slab(asset1, asset2, R, m_prime=None, precision=64, group=None):
                                                  _lib.dptr(np.ascontiguousarray(R)), _lib.dptr(s), precision, klo, nk,
                                                  ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(st)))
     a = _pass(q, (nk, w[1], N[2]), 2, N[2], 1.0, precision)
-    b = _pass(a, (nk, N[1], N[2]), 1, N[1], 1.0, precision)
-    slab = exchange_planes_to_slabs(torch.view_as_real(b), kx_r, y_r, rank, group)
-    slab = torch.view_as_complex(slab.contiguous())
     ny = y_r[rank][1] - y_r[rank][0]
+    if exchange == "auto":
+        dist = _dist()
+        exchange = "fused" if dist.is_initialized() and dist.get_backend(group) == "nccl" else "alltoall"
+    if exchange == "fused":
+        ny_max = max(hi - lo for lo, hi in y_r)
+        buf, hdl = _symm_slab((w[0], ny_max, N[2]), dtype, group)
+        hdl.barrier()  # every rank is done with its slab from the previous call
+        bounds = [lo for lo, _ in y_r] + [y_r[-1][1]]
+        scatter_y_pass(a.contiguous(), N[1], bounds, list(hdl.buffer_ptrs), klo, precision)
+        hdl.barrier()  # every rank's stores into this slab have landed
+        slab = torch.view_as_complex(buf.view(-1)[: 2 * w[0] * ny * N[2]].view(w[0], ny, N[2], 2))
+    else:
+        b = _pass(a, (nk, N[1], N[2]), 1, N[1], 1.0, precision)
+        slab = exchange_planes_to_slabs(torch.view_as_real(b), kx_r, y_r, rank, group)
+        slab = torch.view_as_complex(slab.contiguous())
     scale = 1.0 / (g.node_count * g.cell_volume)
     return _pass(slab, (N[0], ny, N[2]), 0, N[0], scale, precision)
 
