@@ -113,6 +113,12 @@ int gf_affinity_grid(int d, const double *elems, const double *normals, const do
                      double gconst, double lam_in, double lam_out, double max_angle, int max_depth, double eta_floor,
                      void *values_dev, uint8_t *flags_dev, double *stats, void *stream);
 
+/* Winding number at every node of a grid (dims, origin, spacing as in
+ * gf_affinity_grid) into a device array of node_count doubles; the
+ * indicator field of descriptor.py:360-366 is wind >= 0.5 (bit-exact). */
+int gf_winding_grid(int d, const double *elems, int64_t ne, const int32_t *dims, const double *origin, double spacing,
+                    void *wind_dev, void *stream);
+
 /* Slab of the same pipeline for multi-GPU node sharding:
  * owned axis-0 planes [plane0, plane0 + nplanes) of the global grid `dims`,
  * computed together with halo_lo / halo_hi neighbour planes so the

@@ -51,6 +51,8 @@ SIGNATURES = {
                                         ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                         ctypes.c_double, c_vp, c_vp, c_dp, c_vp]),
+    "gf_winding_grid": (ctypes.c_int, [ctypes.c_int, c_dp, ctypes.c_int64, c_i32p, c_dp, ctypes.c_double, c_vp,
+                                       c_vp]),
     "gf_affinity_planes": (ctypes.c_int, [ctypes.c_int, c_dp, c_dp, c_dp, ctypes.c_int64, c_i32p, c_dp,
                                           ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_int, ctypes.c_double, ctypes.c_double,

@@ -408,3 +408,20 @@ def affinity_planes(solid, grid, plane0, nplanes, halo_lo, halo_hi, family, sigm
                                  ctypes.c_void_p(values.data_ptr()), ctypes.c_void_p(flags.data_ptr()), dptr(stats),
                                  ctypes.c_void_p(st)))
     return values, flags, (int(stats[0]), float(stats[1]), float(stats[2]), float(stats[3]))
+
+
+def winding_grid(solid, grid):
+    """Winding numbers at every grid node as a CUDA float64 tensor (no host
+    node-coordinate array; the kernel forms origin + h i itself)."""
+    import torch
+
+    dev = _lib.ensure_device()
+    elems, _, _ = _elements(solid)
+    out = torch.empty(grid.node_count, dtype=torch.float64, device=f"cuda:{dev}")
+    dims = (ctypes.c_int32 * 3)(*(list(grid.dims) + [1] * (3 - len(grid.dims))))
+    origin = np.zeros(3)
+    origin[:grid.dimension] = grid.origin
+    st = torch.cuda.current_stream(out.device).cuda_stream
+    check(LIB.gf_winding_grid(grid.dimension, dptr(elems), len(elems), dims, dptr(origin), float(grid.spacing),
+                              ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st)))
+    return out

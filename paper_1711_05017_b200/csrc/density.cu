@@ -527,6 +527,36 @@ int gf_distance_winding(int d, const double* elems, int64_t ne, const double* P,
   return 0;
 }
 
+int gf_winding_grid(int d, const double* elems, int64_t ne, const int32_t* dims, const double* origin, double spacing,
+                    void* wind_dev, void* stream) {
+  int rc = check_dim(d);
+  if (rc) return rc;
+  GF_CHECK(elems && dims && origin && wind_dev && ne > 0, GF_EINVAL, "bad argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t m = 1;
+  for (int a = 0; a < d; ++a) m *= dims[a];
+  DevBuf de, dx;
+  const int E = d == 3 ? 9 : 4;
+  if ((rc = upload(elems, sizeof(double) * E * ne, de, st))) return rc;
+  GF_CUDA(dx.alloc(sizeof(double) * m));  // the kernel writes distances too
+  PointSource src = {};
+  src.P = nullptr;
+  src.d = d;
+  for (int a = 0; a < 3; ++a) {
+    src.dims[a] = a < d ? dims[a] : 1;
+    src.origin[a] = a < d ? origin[a] : 0.0;
+  }
+  src.spacing = spacing;
+  unsigned grid = (unsigned)ceil_div(m, kThreads);
+  if (d == 3)
+    dist_wind_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dx.p, (double*)wind_dev);
+  else
+    dist_wind_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dx.p, (double*)wind_dev);
+  GF_CUDA(cudaGetLastError());
+  GF_CUDA(cudaStreamSynchronize(st));  // the element and distance buffers go back to the cache
+  return 0;
+}
+
 int gf_sweep(int d, const double* elems, const double* normals, const double* measures, int64_t ne, const double* P,
              const double* xi_eff, int64_t m, double sigma, double gconst, double max_angle, int max_depth,
              double eta_min, double* out_c128, double* resid, int64_t* clamps) {
