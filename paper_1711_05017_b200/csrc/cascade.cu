@@ -447,7 +447,10 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
   }
   a.single = 0;
   // direct gather: 16 x 16 mode patches x runs of L along the run axis
-  int L = a.seg_len > 0 ? a.seg_len : (n_poses >= target_blocks / 2 ? 8 : 4);
+  // many poses: one run spans the whole run axis (fewer run folds and phase
+  // restarts, measured +12 % at w = 96 over L = 8); few poses: short runs so
+  // a pose splits over enough CTAs
+  int L = a.seg_len > 0 ? a.seg_len : (n_poses >= target_blocks / 2 ? 1 << 30 : 4);
   int wmax = a.w[0] > a.w[1] ? a.w[0] : a.w[1];
   if (a.w[2] > wmax) wmax = a.w[2];
   if (a.dim == 2) L = 1;

@@ -7,6 +7,8 @@ import oracle
 from paper_1711_05017_b200 import backend as be, _lib
 from conftest import synthetic_window
 _lib.ensure_device(0)
+if os.environ.get('GF_RUNLEN'):
+    _lib.check(_lib.LIB.gf_set_cascade_run_length(int(os.environ['GF_RUNLEN'])))
 rng = np.random.default_rng(0)
 w = int(sys.argv[1]) if len(sys.argv) > 1 else 96
 W1, W2 = be.DeviceWindow(synthetic_window(rng, w)), be.DeviceWindow(synthetic_window(rng, w))
