@@ -189,6 +189,26 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------------------
+# synthetic poses exactly as the reference's cmd_bench draws them
+# (cli.py:336-346): per pose q ~ N(0, I4) normalised to a rotation, then
+# t ~ U(-span, span)^3, in that order
+
+
+def cmd_bench_poses(n, span, seed=0):
+    rng = np.random.default_rng(seed)
+    Rs, ts = [], []
+    for _ in range(n):
+        w, x, y, z = rng.normal(size=4)
+        nrm = np.sqrt(w * w + x * x + y * y + z * z)
+        w, x, y, z = w / nrm, x / nrm, y / nrm, z / nrm
+        Rs.append([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                   [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                   [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+        ts.append(rng.uniform(-span, span, 3))
+    return np.asarray(Rs), np.asarray(ts)
+
+
+# ---------------------------------------------------------------------------
 # CPU baseline (the reference's compiled kernel, oracle/_ref)
 
 
@@ -472,7 +492,7 @@ class _Asset:
 def measure_stages(args, rank, world, fp32_peak):
     import torch
 
-    import oracle  # pose generator only (cli.py:336-346 restatement); no compute
+    import oracle  # the stages' cpu_baseline legs only (numpy restatements timed on the host)
     from paper_1711_05017_b200 import backend, parallel, scenes
     from paper_1711_05017_b200.descriptor import ComplexField, SampleGrid, affinity_field
     from paper_1711_05017_b200.energy import score_field_device
@@ -489,7 +509,7 @@ def measure_stages(args, rank, world, fp32_peak):
     g3 = SampleGrid(3, (n3,) * 3, (-0.5 * dom3,) * 3, dom3 / n3)
     mk = lambda w: torch.randn((w,) * 3, dtype=torch.complex128, device=dev, generator=gen) * 1e-2  # noqa: E731
     a1, a2 = _Asset(g3, backend.DeviceWindow(mk(w3)), False), _Asset(g3, backend.DeviceWindow(mk(w3)), False)
-    Rs, ts = oracle.bench_poses(args.sweep_poses, 0.25 * dom3, seed=rank)
+    Rs, ts = cmd_bench_poses(args.sweep_poses, 0.25 * dom3, seed=rank)
     c = g3.center()
     t_eff = ts - c + np.einsum("nij,j->ni", Rs, c)
     poses = torch.from_numpy(backend.pack_poses(Rs, t_eff)).to(dev)
@@ -532,7 +552,7 @@ def measure_stages(args, rank, world, fp32_peak):
     n4 = args.field_n
     g4 = SampleGrid(3, (n4,) * 3, (-1.0,) * 3, 2.0 / n4)
     b1, b2 = _Asset(g4, backend.DeviceWindow(mk(n4)), True), _Asset(g4, backend.DeviceWindow(mk(n4)), True)
-    R4, _ = oracle.bench_poses(1, 1.0, seed=1)
+    R4, _ = cmd_bench_poses(1, 1.0, seed=1)
     ms = _time_ms(lambda: score_field_device(b1, b2, R4[0], None, precision=32))
     alg = 24.0 * n4 ** 3  # read both complex64 windows + write the complex64 field
     out["field_C4"] = {
