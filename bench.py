@@ -563,7 +563,11 @@ def measure_stages(args, rank, world, fp32_peak):
                      "frac": alg / (ms * 1e-3) / 1e9 / hbm, "work": "24 B/voxel algorithmic",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                      "traffic": _field_traffic(),
-                     "traffic_unit": "bytes per landscape: product + 3 FFT passes (ncu capture, 512^3)"},
+                     "traffic_unit": "bytes per landscape: product + 3 FFT passes (ncu capture, 512^3)",
+                     "dram_achieved": (_field_traffic() / (ms * 1e-3) / 1e9) if _field_traffic() else None,
+                     "dram_frac": (_field_traffic() / (ms * 1e-3) / 1e9 / hbm) if _field_traffic() else None,
+                     "dram_note": "measured DRAM traffic of the four kernels / this run's time: the HBM "
+                                  "utilisation the north star's >= 50 % target refers to"},
         "scaling_plan": "slab-decomposed across ranks with one all-to-all (parallel.score_field_slab)",
     }
     if rank == 0 and not args.no_cpu:
