@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
 // mapped mailbox and forwards the pose to device memory; the other blocks
 // poll a device word.  No kernel launch per query.
 constexpr unsigned long long kServerStop = ~0ull;
+constexpr int kPollWarps = 4;  // CTA 0 warps polling the host mailbox
 
 template <typename T, bool WRAP>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_server_kernel(CascadeArgs a,
@@ -500,32 +501,54 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
   cluster_red_init(cr);
   unsigned long long last = ctl.start_seq;
   const int tid = threadIdx.x;
+  __shared__ int found;  // CTA 0: a polling warp has the request
   while (true) {
     const unsigned expect = (unsigned)(last + 1);
-    if (tid < 32) {
+    if (tid == 0) found = 0;
+    __syncthreads();
+    // CTA 0 polls the host mailbox with kPollWarps warps whose polls are
+    // staggered in time: a PCIe read takes ~1 us, so several reads in flight
+    // cut the wait between the host's write and its detection
+    const int pollers = blockIdx.x == 0 ? kPollWarps : 1;
+    if (tid < 32 * pollers) {
       // warp 0: lanes 0..24 read the 25 request slots in one instruction and
       // the warp votes; CTA 0 polls the host mailbox (one PCIe round trip per
       // poll, the pose arrives with the tags) and forwards the slots to device
       // memory, the other CTAs poll that copy in L2
-      const int lane = tid;
+      const int lane = tid & 31;
       unsigned long long v = 0;
       bool ok;
+      bool publish = true;
       if (blockIdx.x == 0) {
-        unsigned long long t0;
+        const int pw = tid >> 5;
+        unsigned long long t0, t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {  // stagger the start of warp pw by pw / kPollWarps of a PCIe round trip
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        } while (t1 - t0 < (unsigned long long)(pw * 1000 / kPollWarps));
+        bool mine = false;
         while (true) {
           if (lane < kReqSlots) v = ctl.host_req[lane];
           ok = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
-          if (ok) break;
-          unsigned long long t1;
+          if (ok) {
+            mine = true;
+            break;
+          }
+          const int other = __shfl_sync(0xffffffffu, lane == 0 ? *(volatile int*)&found : 0, 0);
+          if (other) break;  // another warp got it (warp-uniform)
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
           if (t1 - t0 > ctl.idle_timeout_ns) {  // idle: forward a stop request
             v = lane == kReqSlots - 1 ? (((unsigned long long)expect << 32) | 1ull)
                                       : ((unsigned long long)expect << 32);
+            mine = true;
             break;
           }
         }
-        if (lane < kReqSlots) ctl.dev_req[lane] = v;
+        publish = mine;  // only a detecting warp forwards and assembles
+        if (mine) {
+          if (lane < kReqSlots) ctl.dev_req[lane] = v;
+          if (lane == 0) *(volatile int*)&found = 1;
+        }
       } else {
         while (true) {
           if (lane < kReqSlots) v = ctl.dev_req[lane];
@@ -538,8 +561,10 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
       const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, (2 * lane) & 31);
       const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)v, (2 * lane + 1) & 31);
       const unsigned stopw = __shfl_sync(0xffffffffu, (unsigned)v, kReqSlots - 1);
-      if (lane < 12) pose_s[lane] = __hiloint2double((int)hi, (int)lo);
-      if (lane == 0) cur = stopw ? kServerStop : last + 1;
+      if (publish) {  // duplicate detections in CTA 0 write identical values
+        if (lane < 12) pose_s[lane] = __hiloint2double((int)hi, (int)lo);
+        if (lane == 0) cur = stopw ? kServerStop : last + 1;
+      }
     }
     __syncthreads();
     const unsigned long long sq = cur;
