@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
 // mapped mailbox and forwards the pose to device memory; the other blocks
 // poll a device word.  No kernel launch per query.
 constexpr unsigned long long kServerStop = ~0ull;
-constexpr int kPollWarps = 4;  // CTA 0 warps polling the host mailbox
+constexpr int kPollWarps = 2;  // CTA 0 warps polling the host mailbox
 
 template <typename T, bool WRAP>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_server_kernel(CascadeArgs a,
