@@ -504,6 +504,76 @@ def measure_stages(args, rank, world, fp32_peak):
     gen = torch.Generator(device=dev)
     gen.manual_seed(SEED + rank)
 
+    # --- C1: the reference's own CPU case, end to end on real assets: peg-in-hole 64^3, K=16
+    # (m' = 32^3), GPU density -> spectra -> windows, then a 1000-pose insertion trajectory
+    # through the public evaluate(); the reference kernel runs the same windows and poses
+    from paper_1711_05017_b200.energy import Configuration, evaluate
+
+    sc1 = scenes.get_scene("peg_in_hole")
+    m1 = 32 ** 3
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    p1, p2 = sc1.build_assets(64, m_prime=m1)
+    w1c, w1wrap = p1.window(m1)
+    w2c, _ = p2.window(m1)
+    torch.cuda.synchronize()
+    pre_ms = (time.perf_counter() - t0) * 1e3
+    n_traj = 1000
+    zs = np.linspace(0.6, 0.0, n_traj)  # from clear of the block (peg bottom above its top) to seated
+    cfgs = [Configuration(np.eye(3), np.array([0.0, 0.0, z])) for z in zs]
+    from paper_1711_05017_b200.energy import haptic_session
+
+    def run_traj():
+        for cfg in cfgs[:20]:
+            evaluate(p1, p2, cfg, m1)
+        lat, rows = [], []
+        t0 = time.perf_counter()
+        for cfg in cfgs:
+            q0 = time.perf_counter_ns()
+            ev = evaluate(p1, p2, cfg, m1)
+            lat.append((time.perf_counter_ns() - q0) / 1e3)
+            rows.append(np.concatenate([[ev.energy], ev.force, ev.torque]))
+        dt = time.perf_counter() - t0
+        lat.sort()
+        return n_traj / dt, lat[len(lat) // 2], lat[min(len(lat) - 1, int(0.99 * len(lat)))], rows
+
+    with haptic_session(p1, p2, m1):
+        rate_s, p50_s, p99_s, res1 = run_traj()
+    rate_l, p50_l, p99_l, _ = run_traj()
+    out["trajectory_C1"] = {
+        "workload": "peg-in-hole (64-gon cylinder peg, bored block) 64^3, K=16 (m'=32768), 1000-pose "
+                    "insertion trajectory through evaluate(); assets built on the GPU from the meshes",
+        "precompute_ms": pre_ms, "poses_per_s": rate_s, "p50_us": p50_s, "p99_us": p99_s,
+        "path": "evaluate() inside haptic_session (resident query grid)",
+        "launch_path": {"poses_per_s": rate_l, "p50_us": p50_l, "p99_us": p99_l},
+        "precision": backend.precision()}
+    if rank == 0 and not args.no_cpu:
+        core = reference_core()
+        g1 = p1.grid
+        C1h, C2h = np.asarray(w1c), np.asarray(w2c)
+        c1 = g1.center()
+        dcell1 = 1.0 / (g1.node_count * g1.cell_volume)
+        idx = np.linspace(0, n_traj - 1, 100).astype(int)
+        t0 = time.perf_counter()
+        refs = [core.cascade_3d(C1h, C2h, bool(w1wrap), *g1.delta_omega(), dcell1, np.eye(3),
+                                np.ascontiguousarray(cfgs[i].translation), c1) for i in idx]
+        dt = time.perf_counter() - t0
+        ref_rows = np.array([np.concatenate([[-r[0].real], r[1:4].real, r[4:7].real]) for r in refs])
+        got = np.array(res1)[idx]
+        # parity as BASELINE.md states it: |new - ref| <= 1e-4 max(|ref|, L1), L1 = dcell sum |summand|
+        l1 = np.array([np.abs(oracle.cascade_term_scales(C1h, C2h, bool(w1wrap), g1.delta_omega(), dcell1,
+                                                         np.eye(3), cfgs[i].translation, c1))
+                       for i in idx])
+        denom = np.maximum(np.abs(ref_rows), l1)
+        out["trajectory_C1"]["max_err_over_tolerance_scale"] = float(np.max(np.abs(got - ref_rows) / denom))
+        out["trajectory_C1"]["tolerance"] = "1e-4 of max(|ref|, L1) (BASELINE.md section 2)"
+        out["trajectory_C1"]["cpu_baseline"] = {
+            "value": len(idx) / dt, "unit": "poses/s", "cores": 1, "kind": "reference",
+            "sample": f"{len(idx)} trajectory poses through _core.cascade_3d (oracle/_ref) on the same "
+                      "windows, single thread"}
+    del p1, p2
+    torch.cuda.empty_cache()
+
     # --- C3: batched pose sweep, gear-pair grid 256^3, K=48 (w=96), cmd_bench poses
     n3, w3, dom3 = 256, 96, 5.42
     g3 = SampleGrid(3, (n3,) * 3, (-0.5 * dom3,) * 3, dom3 / n3)
