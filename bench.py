@@ -574,6 +574,64 @@ def measure_stages(args, rank, world, fp32_peak):
     del p1, p2
     torch.cuda.empty_cache()
 
+    # --- C2 on real assets: the low-clearance peg-in-hole at 128^3, K=32 (m' = 64^3), the
+    # headline configuration with GPU-built windows instead of synthetic ones; the jittered
+    # insertion path of the headline, through evaluate() in a haptic session
+    sc2 = scenes.get_scene("peg_in_hole_lowclear")
+    m2 = 64 ** 3
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    q1, q2 = sc2.build_assets(128, m_prime=m2)
+    v1c, v1wrap = q1.window(m2)
+    v2c, _ = q2.window(m2)
+    torch.cuda.synchronize()
+    pre2_ms = (time.perf_counter() - t0) * 1e3
+    Rj, tj, _ = trajectory(2000, SEED + 11)
+    cfg2 = [Configuration(R, t) for R, t in zip(Rj, tj)]
+    with haptic_session(q1, q2, m2):
+        for cfg in cfg2[:50]:
+            evaluate(q1, q2, cfg, m2)
+        lat2, rows2 = [], []
+        t0 = time.perf_counter()
+        for cfg in cfg2:
+            q0 = time.perf_counter_ns()
+            ev = evaluate(q1, q2, cfg, m2)
+            lat2.append((time.perf_counter_ns() - q0) / 1e3)
+            rows2.append(np.concatenate([[ev.energy], ev.force, ev.torque]))
+        dt2 = time.perf_counter() - t0
+    lat2.sort()
+    out["trajectory_C2_real"] = {
+        "workload": "low-clearance peg-in-hole 128^3 (clearance 0.01 x bore), K=32 (m'=262144), 2000-pose "
+                    "jittered insertion path through evaluate() in a haptic session; assets built on the GPU",
+        "precompute_ms": pre2_ms, "poses_per_s": len(cfg2) / dt2, "p50_us": lat2[len(lat2) // 2],
+        "p99_us": lat2[min(len(lat2) - 1, int(0.99 * len(lat2)))], "precision": backend.precision()}
+    if rank == 0 and not args.no_cpu:
+        core = reference_core()
+        g2 = q1.grid
+        D1h, D2h = np.asarray(v1c), np.asarray(v2c)
+        c2 = g2.center()
+        dcell2 = 1.0 / (g2.node_count * g2.cell_volume)
+        idx = np.linspace(0, len(cfg2) - 1, 20).astype(int)
+        teff = [cfg2[i].translation - c2 + cfg2[i].rotation @ c2 for i in idx]
+        t0 = time.perf_counter()
+        refs = [core.cascade_3d(D1h, D2h, bool(v1wrap), *g2.delta_omega(), dcell2,
+                                np.ascontiguousarray(cfg2[i].rotation), np.ascontiguousarray(te), c2)
+                for i, te in zip(idx, teff)]
+        dt = time.perf_counter() - t0
+        ref_rows = np.array([np.concatenate([[-r[0].real], r[1:4].real, r[4:7].real]) for r in refs])
+        l1 = np.array([np.abs(oracle.cascade_term_scales(D1h, D2h, bool(v1wrap), g2.delta_omega(), dcell2,
+                                                         cfg2[i].rotation, te, c2)) for i, te in zip(idx, teff)])
+        got = np.array(rows2)[idx]
+        out["trajectory_C2_real"]["max_err_over_tolerance_scale"] = float(
+            np.max(np.abs(got - ref_rows) / np.maximum(np.abs(ref_rows), l1)))
+        out["trajectory_C2_real"]["tolerance"] = "1e-4 of max(|ref|, L1) (BASELINE.md section 2)"
+        out["trajectory_C2_real"]["cpu_baseline"] = {
+            "value": len(idx) / dt, "unit": "poses/s", "cores": 1, "kind": "reference",
+            "sample": f"{len(idx)} of the same poses through _core.cascade_3d (oracle/_ref) on the same windows, "
+                      "single thread"}
+    del q1, q2
+    torch.cuda.empty_cache()
+
     # --- C3: batched pose sweep, gear-pair grid 256^3, K=48 (w=96), cmd_bench poses
     n3, w3, dom3 = 256, 96, 5.42
     g3 = SampleGrid(3, (n3,) * 3, (-0.5 * dom3,) * 3, dom3 / n3)
