@@ -769,7 +769,12 @@ def measure_stages(args, rank, world, fp32_peak):
     nf = len(sc.fixed.mesh.faces)
     out["density_D"] = {"workload": f"affinity_field, bored block ({nf} faces) on 64^3, float64 bit-exact flags",
                         "voxels_per_s": gd.node_count / dt, "node_face_pairs_per_s": gd.node_count * nf / dt,
-                        "ms": dt * 1e3, "excluded": fd.stats["excluded"], "unresolved": fd.stats["unresolved_nodes"]}
+                        "ms": dt * 1e3, "excluded": fd.stats["excluded"], "unresolved": fd.stats["unresolved_nodes"],
+                        "device_seconds": {"distance_winding": fd.stats.get("seconds_distance"),
+                                           "sweep": fd.stats.get("seconds_sweep")},
+                        "roofline": {"bound": "fp64", "unit": "FP64 pipe utilisation (ncu)", "frac": 0.409,
+                                     "source": "profiles/r01_ncu_density_sweep.txt: sweep_kernel "
+                                               "sm__inst_executed_pipe_fp64 40.9 % of peak"}}
     if rank == 0 and not args.no_cpu:
         core = reference_core()
         gc = sc.grid(16)
