@@ -366,6 +366,25 @@ def run_engine(args):
     lat1, dt1 = e2e_loop()  # no server: one single-query kernel launch per call
     e2e_value = args.e2e_queries * world / e2e_s
 
+    # the float64 engine (the reference's own tolerances) on the same loop, for reference
+    fp64_mode = None
+    if prec == "fp32":
+        def e2e64():
+            lat64 = []
+            for i in range(50):
+                backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision="fp64")
+            for i in range(50, 50 + args.e2e_queries):
+                q0 = time.perf_counter_ns()
+                backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision="fp64")
+                lat64.append((time.perf_counter_ns() - q0) / 1e3)
+            return sorted(lat64)
+
+        with backend.HapticServer(W1, W2, False, dom, dcell, center, precision="fp64"):
+            l64 = e2e64()
+        fp64_mode = {"e2e_p50_us": statistics.median(l64), "e2e_p99_us": l64[min(len(l64) - 1, int(0.99 * len(l64)))],
+                     "e2e_queries_per_s": 1e6 / float(np.mean(l64)),
+                     "note": "same session loop in the float64 engine (reference tolerances 1e-9..1e-12)"}
+
     def pct(xs, p):
         return xs[min(len(xs) - 1, int(p * len(xs)))]
 
@@ -417,6 +436,7 @@ def run_engine(args):
                          "work": f"240 flops x live modes ({live:.3f} x {W ** 3}) per launch",
                          "peak_source": "FMA-chain kernel measured in this run (gf_measure_fma_peak)"},
             "cpu_baseline": cpu,
+            "fp64_engine": fp64_mode,
             "gpu_launches": QUERIES_PER_STEP * args.steps,
             "clocks": clk.summary(),
             "stages": stages,

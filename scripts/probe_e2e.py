@@ -6,6 +6,8 @@ import numpy as np, torch
 from paper_1711_05017_b200 import backend as be, _lib
 from conftest import synthetic_window, random_rotation
 _lib.ensure_device(0)
+if os.environ.get('GF_PREC'):
+    be.set_precision(os.environ['GF_PREC'])
 if os.environ.get('GF_TILE'):
     _lib.check(_lib.LIB.gf_set_cascade_tile(int(os.environ['GF_TILE'])))
 rng = np.random.default_rng(0)
@@ -27,7 +29,7 @@ f = _lib.LIB.gf_cascade_fast
 lat = []
 for i in range(n):
     q.arg[:9] = Rs[i].ravel(); q.arg[9:12] = ts[i]
-    t0 = time.perf_counter(); f(W1.handle, W2.handle, 0, q.pd, 1.0, q.pR, q.pt, q.pc, 32, q.pout); lat.append((time.perf_counter() - t0) * 1e6)
+    t0 = time.perf_counter(); f(W1.handle, W2.handle, 0, q.pd, 1.0, q.pR, q.pt, q.pc, 64 if be.precision() == 'fp64' else 32, q.pout); lat.append((time.perf_counter() - t0) * 1e6)
 print("B raw gf_cascade (ctypes) ", pct(lat))
 lat = []
 for i in range(n):
