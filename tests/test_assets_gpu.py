@@ -66,3 +66,20 @@ def test_precompute_matches_reference_directory(tmp_path):
         _check_evals(fixed, moving, 1e-5)
     finally:
         backend.set_precision("fp32")
+
+
+def test_solid_manifests_merge_and_mismatch(tmp_path):
+    """Per-solid precompute merges fixed and moving parts into one manifest
+    when grid and kernel agree (cli.py:208-216), and refuses otherwise."""
+    out = tmp_path / "m3"
+    assets.precompute(str(out), 8, solid="box", role="fixed", domain=6.0)
+    man = assets.precompute(str(out), 8, solid="icosphere", role="moving", domain=6.0)
+    assert set(man["parts"]) == {"fixed", "moving"}
+    assert man["parts"]["fixed"]["solid_kind"] == "file"  # named by role, as the reference does
+    _, fixed, moving = assets.load_assets(str(out))
+    ev = evaluate(fixed, moving, Configuration(np.eye(3), [0.0, 0.0, 0.75]))
+    assert ev.force.shape == (3,) and ev.torque.shape == (3,) and np.isfinite(ev.energy)
+    out2 = tmp_path / "m3b"
+    assets.precompute(str(out2), 8, solid="box", role="fixed", domain=6.0)
+    with pytest.raises(ValueError, match="different grid or kernel"):
+        assets.precompute(str(out2), 8, solid="icosphere", role="moving", domain=8.0)
