@@ -131,16 +131,17 @@ int gf_affinity_planes(int d, const double *elems, const double *normals, const 
                        double lam_out, double max_angle, int max_depth, double eta_floor, void *values_dev,
                        uint8_t *flags_dev, double *stats, void *stream);
 
-/* Multi-GPU landscape: the y inverse pass of this rank's window x-planes
- * (shape_in = (nk, L1, N2), centred input when in_centered, node-ordered
- * output of length n = y_bounds[nranks]) fused with the slab exchange: line
- * element (x, y, z) is stored into rank s's y-slab (w0, ny_s, N2) at plane
- * x_off + x, row y - y_bounds[s]; dst_ptrs[s] is that slab's device address
- * (a peer mapping on another GPU, e.g. a symmetric-memory buffer).  Replaces
- * fft pass + all-to-all of parallel.score_field_slab. */
-int gf_fft_pass_scatter(int precision, const void *in, const int32_t *shape_in, int n, int in_centered, int sign,
-                        double in_phase, double scale, int nranks, const int32_t *y_bounds, const uint64_t *dst_ptrs,
-                        int x_off, void *stream);
+/* Multi-GPU slab exchange fused into an axis-1 pass: the FFT of this
+ * rank's lines (shape_in = (nk, L1, N2), length-n transform, input / output
+ * node-ordered or DC-centred exactly as gf_fft_pass, out_len rows out) with
+ * output row y of plane x stored into rank s's y-slab (planes, ny_s, N2) at
+ * plane x_off + x, row y - y_bounds[s] (y_bounds tile [0, out_len));
+ * dst_ptrs[s] is that slab's device address (a peer mapping on another GPU,
+ * e.g. a symmetric-memory buffer).  Replaces pass + all-to-all in
+ * parallel.score_field_slab and forward_window_slab (W1). */
+int gf_fft_pass_scatter(int precision, const void *in, const int32_t *shape_in, int n, int in_centered, int out_len,
+                        int out_centered, int sign, double in_phase, double out_phase, double scale, int nranks,
+                        const int32_t *y_bounds, const uint64_t *dst_ptrs, int x_off, void *stream);
 
 /* Spectra (stage 2) and landscapes (stage 4) ------------------------------ */
 

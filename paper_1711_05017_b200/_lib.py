@@ -59,8 +59,9 @@ SIGNATURES = {
                                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                           ctypes.c_double, c_vp, c_vp, c_dp, c_vp]),
     "gf_fft_pass_scatter": (ctypes.c_int, [ctypes.c_int, c_vp, c_i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                           ctypes.c_double, ctypes.c_double, ctypes.c_int, c_i32p,
-                                           ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, c_vp]),
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_int, c_i32p, ctypes.POINTER(ctypes.c_uint64),
+                                           ctypes.c_int, c_vp]),
     "gf_fft_pass": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_i32p, c_i32p, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                    ctypes.c_double, c_vp]),

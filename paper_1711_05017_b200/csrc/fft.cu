@@ -586,14 +586,25 @@ __global__ void __launch_bounds__(B * (N / 8)) fft_scatter_kernel(FftArgs a, Sca
   cx<T>* line = buf + b * LD;
   fft_line<T, N>(v, line, j, tw, a.sign);
   if (!live) return;
+  const int Lout = a.shape_out[1], hout = Lout / 2;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const int y = j + r * TPL;  // node order
+    const int pos = j + r * TPL;
+    int y, m;  // output row and mode number of FFT position pos
+    if (a.out_centered) {
+      m = pos < N / 2 ? pos : pos - N;
+      y = m + hout;
+      if (y < 0 || y >= Lout) continue;  // truncated away
+    } else {
+      m = pos;
+      y = pos;
+    }
     int s = 0;
     while (s + 1 < so.nranks && y >= so.ybound[s + 1]) ++s;
     const int ny = so.ybound[s + 1] - so.ybound[s];
-    cx<T> val = line[sidx<T>(y)];
+    cx<T> val = line[sidx<T>(pos)];
     val = mk<T>(val.re * (T)a.scale, val.im * (T)a.scale);
+    if (a.out_phase_kind) val = val * phase_factor<T>(a.out_phase_kind, a.out_phase, m);
     cx<T>* dst = reinterpret_cast<cx<T>*>(so.dst[s]);
     dst[((int64_t)(so.x_off + o) * ny + (y - so.ybound[s])) * s2 + p] = val;
   }
@@ -916,15 +927,17 @@ extern "C" int gf_fft_pass(int precision, const void* in, void* out, const int32
 }
 
 extern "C" int gf_fft_pass_scatter(int precision, const void* in, const int32_t* shape_in, int n, int in_centered,
-                                   int sign, double in_phase, double scale, int nranks, const int32_t* y_bounds,
-                                   const uint64_t* dst_ptrs, int x_off, void* stream) {
+                                   int out_len, int out_centered, int sign, double in_phase, double out_phase,
+                                   double scale, int nranks, const int32_t* y_bounds, const uint64_t* dst_ptrs,
+                                   int x_off, void* stream) {
   GF_CHECK(in && shape_in && y_bounds && dst_ptrs, GF_EINVAL, "null argument");
   GF_CHECK(nranks >= 1 && nranks <= kMaxScatter, GF_EINVAL, "1 to 8 destination ranks");
   GF_CHECK(n >= 8 && n <= 1024 && (n & (n - 1)) == 0, GF_EINVAL, "FFT length must be a power of two in [8, 1024]");
   GF_CHECK(precision == 32 || precision == 64, GF_EINVAL, "precision must be 32 or 64");
   GF_CHECK(sign == -1 || sign == 1, GF_EINVAL, "sign must be -1 or +1");
   GF_CHECK(shape_in[1] <= n && (in_centered || shape_in[1] == n), GF_EINVAL, "bad line length");
-  GF_CHECK(y_bounds[0] == 0 && y_bounds[nranks] == n, GF_EINVAL, "y slabs must tile [0, n)");
+  GF_CHECK(out_len <= n && (out_centered || out_len == n), GF_EINVAL, "bad output length");
+  GF_CHECK(y_bounds[0] == 0 && y_bounds[nranks] == out_len, GF_EINVAL, "y slabs must tile the output rows");
   for (int r = 0; r < nranks; ++r) {
     GF_CHECK(y_bounds[r + 1] >= y_bounds[r], GF_EINVAL, "y slab bounds must be non-decreasing");
     GF_CHECK(dst_ptrs[r] != 0 || y_bounds[r + 1] == y_bounds[r], GF_EINVAL, "null destination slab");
@@ -938,14 +951,16 @@ extern "C" int gf_fft_pass_scatter(int precision, const void* in, const int32_t*
   GF_CHECK(a.tw != nullptr, GF_ENOMEM, "twiddle table allocation failed");
   for (int k = 0; k < 3; ++k) a.shape_in[k] = shape_in[k];
   a.shape_out[0] = shape_in[0];
-  a.shape_out[1] = n;
+  a.shape_out[1] = out_len;
   a.shape_out[2] = shape_in[2];
   a.axis = 1;
   a.in_centered = in_centered;
-  a.out_centered = 0;
+  a.out_centered = out_centered;
   a.sign = sign;
   a.in_phase = in_phase;
   a.in_phase_kind = phase_kind(in_phase);
+  a.out_phase = out_phase;
+  a.out_phase_kind = phase_kind(out_phase);
   a.scale = scale;
   ScatterOut so = {};
   so.nranks = nranks;

@@ -10,10 +10,11 @@
   the data by output y-slabs (each rank gets every x-plane of its y-range),
   and the last pass inverts along x (w0 -> N0).  Rank r ends with the
   landscape rows y in [c_r, d_r): an (N0, d_r - c_r, N2) slab.
-* Forward window (W1) of a node-sharded field: the z and y passes (pruned
-  N -> w) run on each rank's x-planes, one all-to-all re-slices the
-  (nx, w, w) planes into window y-slabs, and the x pass (N0 -> w) finishes;
-  only the (2K)^3 window ever crosses the fabric.
+* Forward window (W1) of a node-sharded field: the z pass runs on each
+  rank's x-planes, the y pass (pruned N -> w) stores straight into the
+  window y-slabs of the destination ranks (NCCL: symmetric memory; gloo: an
+  all-to-all after the pass), and the x pass (N0 -> w) finishes; only the
+  (2K)^3 window ever crosses the fabric.
 * Density (D1/D2): node slabs along axis 0, one per rank, triangles
   replicated; each rank also computes one halo plane per interior side so
   the excluded-node neighbour fill is exact across slab boundaries (the
@@ -177,16 +178,23 @@ def _symm_slab(shape, dtype, group):
     return _SYMM[key]
 
 
-def scatter_y_pass(a, n1, bounds, dst_ptrs, x_off, precision):
-    """The y inverse pass of this rank's planes `a` (nk, w1, N2), stored
-    straight into the destination ranks' y-slabs (gf_fft_pass_scatter)."""
+def scatter_y_pass(a, n1, bounds, dst_ptrs, x_off, precision, forward=False):
+    """An axis-1 pass of this rank's planes `a` (nk, L1, N2) stored straight
+    into the destination ranks' y-slabs (gf_fft_pass_scatter).  Inverse
+    (landscape): centred window in, n1 node rows out.  forward=True (window):
+    node rows in, the centred window of bounds[-1] rows out with the (-1)^m
+    centre phase, as spectral.forward_window."""
     import torch
 
     si = (ctypes.c_int32 * 3)(*a.shape)
     yb = (ctypes.c_int32 * len(bounds))(*bounds)
     dp = (ctypes.c_uint64 * len(dst_ptrs))(*dst_ptrs)
     st = torch.cuda.current_stream(a.device).cuda_stream
-    _lib.check(_lib.LIB.gf_fft_pass_scatter(precision, ctypes.c_void_p(a.data_ptr()), si, int(n1), 1, 1, 0.0, 1.0,
+    if forward:
+        args = (0, int(bounds[-1]), 1, -1, 0.0, 0.5)
+    else:
+        args = (1, int(n1), 0, 1, 0.0, 0.0)
+    _lib.check(_lib.LIB.gf_fft_pass_scatter(precision, ctypes.c_void_p(a.data_ptr()), si, int(n1), *args, 1.0,
                                             len(dst_ptrs), yb, dp, int(x_off), ctypes.c_void_p(st)))
 
 
@@ -367,7 +375,7 @@ def window_outer_pass(slab, dims, w, cell_volume, precision=64):
     return _wpass(slab, (w, slab.shape[1], w), 0, dims[0], cell_volume, precision)
 
 
-def forward_window_slab(local, grid, w, precision=64, group=None, gather=True):
+def forward_window_slab(local, grid, w, precision=64, group=None, gather=True, exchange="auto"):
     """spectral.forward_window for a field sharded by axis-0 planes
     (shard_range layout, local = this rank's (nx, N1, N2) CUDA complex
     planes).  Bit-identical to the single-GPU window: the same 1-D passes on
@@ -384,9 +392,24 @@ def forward_window_slab(local, grid, w, precision=64, group=None, gather=True):
     local = local.reshape(-1, N[1], N[2]).to(dtype)
     x_r = [shard_range(N[0], r, world) for r in range(world)]
     wy_r = [shard_range(w, r, world) for r in range(world)]
-    b = window_inner_passes(local, N, w, precision)
-    slab = exchange_planes_to_slabs(torch.view_as_real(b), x_r, wy_r, rank, group)
-    slab = torch.view_as_complex(slab.contiguous())
+    if exchange == "auto":
+        dist = _dist()
+        exchange = "fused" if dist.is_initialized() and dist.get_backend(group) == "nccl" else "alltoall"
+    if exchange == "fused":  # y pass stores straight into the peers' window y-slabs
+        nx = local.shape[0]
+        a = _wpass(local, (nx, N[1], w), 2, N[2], 1.0, precision)
+        wy_max = max(hi - lo for lo, hi in wy_r)
+        buf, hdl = _symm_slab((N[0], wy_max, w), dtype, group)
+        hdl.barrier()
+        bounds = [lo for lo, _ in wy_r] + [wy_r[-1][1]]
+        scatter_y_pass(a.contiguous(), N[1], bounds, list(hdl.buffer_ptrs), x_r[rank][0], precision, forward=True)
+        hdl.barrier()
+        wy = wy_r[rank][1] - wy_r[rank][0]
+        slab = torch.view_as_complex(buf.view(-1)[: 2 * N[0] * wy * w].view(N[0], wy, w, 2))
+    else:
+        b = window_inner_passes(local, N, w, precision)
+        slab = exchange_planes_to_slabs(torch.view_as_real(b), x_r, wy_r, rank, group)
+        slab = torch.view_as_complex(slab.contiguous())
     out = window_outer_pass(slab, N, w, grid.cell_volume, precision)
     if not gather:
         return out, wy_r[rank]

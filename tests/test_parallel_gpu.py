@@ -109,6 +109,11 @@ def test_fused_exchange_through_symmetric_memory_single_rank(assets):
         fused = parallel.score_field_slab(a1, a2, R, None, exchange="fused")
         plain = parallel.score_field_slab(a1, a2, R, None, exchange="alltoall")
         assert torch.equal(fused, plain)
+        g = a1.grid
+        x = torch.randn(g.dims, dtype=torch.complex128, device="cuda")
+        wf = parallel.forward_window_slab(x, g, 16, exchange="fused")
+        wa = parallel.forward_window_slab(x, g, 16, exchange="alltoall")
+        assert torch.equal(wf, wa)
     finally:
         parallel._SYMM.clear()
         dist.destroy_process_group()

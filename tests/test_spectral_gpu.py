@@ -127,5 +127,13 @@ def test_forward_window_node_slabs_bit_identical(N, w, prec):
             outs.append(parallel.window_outer_pass(slab, N, w, g.cell_volume, prec))
         got = torch.cat(outs, dim=1)
         assert torch.equal(got, want)
+        # fused variant: each rank's y pass stores into every rank's window y-slab
+        slabs = [torch.zeros((N[0], hi - lo, w), dtype=dt, device="cuda") for lo, hi in wy_r]
+        bounds = [lo for lo, _ in wy_r] + [wy_r[-1][1]]
+        for lo, hi in x_r:
+            a = parallel._wpass(x[lo:hi].contiguous(), (hi - lo, N[1], w), 2, N[2], 1.0, prec)
+            parallel.scatter_y_pass(a, N[1], bounds, [t.data_ptr() for t in slabs], lo, prec, forward=True)
+        fused = torch.cat([parallel.window_outer_pass(sl, N, w, g.cell_volume, prec) for sl in slabs], dim=1)
+        assert torch.equal(fused, want)
     # world 1 through the public entry (no process group)
     assert torch.equal(parallel.forward_window_slab(x, g, w, precision=prec), want)
