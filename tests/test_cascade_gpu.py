@@ -122,3 +122,35 @@ def test_haptic_server_matches_one_shot(be):
         assert srv.key not in be._servers
         for g, w_ in zip(got, want):
             np.testing.assert_array_equal(g, w_)  # same kernel body, same reduction order
+
+
+def test_haptic_server_2d_fp64_and_idle_timeout(be):
+    import time
+
+    from paper_1711_05017_b200._lib import EngineError
+
+    rng = np.random.default_rng(22)
+    # 2D windows, float64 engine: the resident grid answers bit for bit like the launch path
+    C1, C2 = synthetic_window(rng, 32, d=2), synthetic_window(rng, 32, d=2)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom, c = (0.2, 0.2), np.array([0.1, -0.2])
+    poses = []
+    for _ in range(10):
+        th = rng.uniform(0, 2 * np.pi)
+        poses.append((np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]]), rng.uniform(-1, 1, 2)))
+    want = [be.cascade(W1, W2, False, dom, 0.3, R, t, c, precision="fp64") for R, t in poses]
+    with be.HapticServer(W1, W2, False, dom, 0.3, c, precision="fp64"):
+        got = [be.cascade(W1, W2, False, dom, 0.3, R, t, c, precision="fp64") for R, t in poses]
+    for g, w_ in zip(got, want):
+        assert g.shape == (4,)
+        np.testing.assert_array_equal(g, w_)
+    # idle timeout: the grid exits by itself; a query then raises, a new session works
+    srv = be.HapticServer(W1, W2, False, dom, 0.3, c, precision="fp64", idle_timeout_s=0.05)
+    time.sleep(0.3)
+    with pytest.raises(EngineError, match="idle timeout"):
+        be.check(be.LIB.gf_server_query(srv.id, *[be.dptr(np.ascontiguousarray(x)) for x in
+                                                  (np.eye(2), np.zeros(2), np.zeros(14))]))
+    srv.stop()
+    with be.HapticServer(W1, W2, False, dom, 0.3, c, precision="fp64"):
+        again = be.cascade(W1, W2, False, dom, 0.3, poses[0][0], poses[0][1], c, precision="fp64")
+    np.testing.assert_array_equal(again, want[0])
