@@ -25,22 +25,17 @@ from __future__ import annotations
 import hashlib
 import json
 import os
-import struct
 import time
 
 import numpy as np
 
-from . import _lib
+from . import _lib, containers
 from .descriptor import KernelSpec, SampleGrid, affinity_field, write_field
 from .energy import PartAsset
 from .spectral import Spectrum, TruncatedSpectrum, VectorSpectrum, read_spectrum, truncate, write_spectrum
 
 __all__ = ["precompute", "precompute_part", "load_manifest", "load_assets", "read_spectrum_device", "sha256_file",
            "BUILTIN_SOLIDS"]
-
-_MAGIC = b"GSPC"
-_VERSION = 1
-
 
 def _builtin_solids():
     from .scenes import box_mesh, icosphere, lbracket
@@ -83,16 +78,8 @@ def load_manifest(path):
 
 
 def _read_header(fh):
-    if fh.read(4) != _MAGIC:
-        raise ValueError("not a GSPC file")
-    version, d = struct.unpack("<II", fh.read(8))
-    if version != _VERSION:
-        raise ValueError(f"unsupported GSPC version {version}")
-    dims = struct.unpack(f"<{d}I", fh.read(4 * d))
-    (spacing,) = struct.unpack("<d", fh.read(8))
-    origin = struct.unpack(f"<{d}d", fh.read(8 * d))
-    (m_prime,) = struct.unpack("<Q", fh.read(8))
-    return SampleGrid(d, tuple(dims), tuple(origin), spacing), int(m_prime)
+    d, dims, origin, spacing, count = containers.unpack_header(fh, b"GSPC")
+    return SampleGrid(d, dims, origin, spacing), int(count)
 
 
 def read_spectrum_device(path):
