@@ -210,9 +210,9 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double *domega, do
 int gf_server_query(uint64_t server_id, const double *R, const double *t_eff, double *out);
 int gf_server_stop(uint64_t server_id);
 
-/* Tuning knobs for experiments: kernel variant (0 = u-space tiled, the
- * default; 1 = direct gather) and the direct variant's run length along kz
- * per thread (0 = auto). */
+/* Tuning knobs for experiments: kernel variant (1 = direct gather, the
+ * default; 0 = u-space tiled), the tiled variant's tile side, and the direct
+ * variant's run length along the run axis per thread (0 = auto). */
 int gf_set_cascade_variant(int variant);
 int gf_set_cascade_tile(int tile);
 /* Debug: per-CTA phase timestamps (globaltimer ns) of the single-query kernel
