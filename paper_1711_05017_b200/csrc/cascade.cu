@@ -37,6 +37,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 namespace gf {
 
 namespace {
@@ -152,6 +154,12 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
   __shared__ double wsum[kWarps][kNumMoments];
   __shared__ double red[kNumMoments];
   __shared__ unsigned ticket;
+  __shared__ int tie_dep[3];
+  // tie table (lattice-aligned poses, see cascade_single.cu): (floor, frac)
+  // of the reference index of axis c at [offset(b) + k_b] when column c of R
+  // has its single nonzero in row b
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  cx<T>* ttab = reinterpret_cast<cx<T>*>(dyn_smem);
 
   const int bpp = a.blocks_per_pose;
   const int64_t pose = a.pose_offset + blockIdx.x / bpp;
@@ -188,7 +196,29 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
       orient.step_im[ax] = s;
     }
   }
+  if (tid == 32) {
+    for (int ax = 0; ax < 3; ++ax) {
+      const double* R = ps.R;
+      const int nz = (R[ax] != 0.0) + (R[3 + ax] != 0.0) + (R[6 + ax] != 0.0);
+      tie_dep[ax] = nz != 1 ? -1 : (R[ax] != 0.0 ? 0 : (R[3 + ax] != 0.0 ? 1 : 2));
+    }
+  }
   __syncthreads();
+  if (tie_dep[0] >= 0 || tie_dep[1] >= 0 || tie_dep[2] >= 0) {
+    for (int i = tid; i < w0 + w1 + w2; i += kThreads) {
+      const int b = i < w0 ? 0 : (i < w0 + w1 ? 1 : 2);
+      const int k = i - (b == 0 ? 0 : (b == 1 ? w0 : w0 + w1));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (tie_dep[c] != b) continue;
+        const double ue = exact_u(ps, a.dom, c, b == 0 ? k : w0 / 2, b == 1 ? k : w1 / 2, b == 2 ? k : w2 / 2, w0 / 2,
+                                  w1 / 2, w2 / 2, c == 0 ? w0 / 2 : (c == 1 ? w1 / 2 : w2 / 2));
+        const double fe = floor(ue);
+        ttab[i] = mk<T>((T)fe, (T)(ue - fe));
+      }
+    }
+    __syncthreads();
+  }
 
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
   const int64_t sy = (int64_t)(w2 + 1), sx = (int64_t)(w1 + 2) * (w2 + 1);
@@ -208,9 +238,14 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
   const int dq = 8 * (warp >> 2) + (lane >> 2);
   const int units = orient.nP * orient.nQ * orient.nR;
 
+  const int tmask = (tie_dep[0] >= 0 ? 1 : 0) | (tie_dep[1] >= 0 ? 2 : 0) | (a.dim == 3 && tie_dep[2] >= 0 ? 4 : 0);
   Acc26<T> acc;
   acc.zero();
 
+  // the unit loop, compiled twice: with the tie table (lattice-aligned pose)
+  // and without it (generic pose: no table branch in the mode loop)
+  auto unit_loop = [&](auto ties_c) {
+  constexpr bool TIES = decltype(ties_c)::value;
   for (int unit = blk; unit < units; unit += bpp) {
     const int ir = unit % orient.nR;
     const int iq = (unit / orient.nR) % orient.nQ;
@@ -243,18 +278,23 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
       const T j = (T)(kr - kr0);
       T u[3] = {fma(j, mr0, u0x), fma(j, mr1, u0y), fma(j, mr2, u0z)};
       T fl[3], f[3];
+      bool tie[3];
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         fl[ax] = floor(u[ax]);
         f[ax] = u[ax] - fl[ax];
+        tie[ax] = !(TIES && ((tmask >> ax) & 1)) && (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
       }
-      const bool tz = a.dim == 3 && (f[2] < eps || f[2] > (T)1 - eps);
-      if (f[0] < eps || f[0] > (T)1 - eps || f[1] < eps || f[1] > (T)1 - eps || tz) {
-        // reference float64 floor decision for near-integer indices
+      if (TIES || tie[0] || tie[1] || tie[2]) {
         const int kkx = r == 0 ? kr : kx, kky = r == 1 ? kr : ky, kkz = r == 2 ? kr : kz0;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-          if ((ax < 2 || tz) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
+          if (TIES && ((tmask >> ax) & 1)) {  // lattice-aligned axis: tabulated reference floor / frac
+            const int dep = tie_dep[ax];
+            const cx<T> e = ttab[dep == 0 ? kkx : (dep == 1 ? w0 + kky : w0 + w1 + kkz)];
+            fl[ax] = e.re;
+            f[ax] = e.im;
+          } else if (tie[ax]) {  // reference float64 floor decision for near-integer indices
             double ue = exact_u(ps, a.dom, ax, kkx, kky, kkz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
             double fe = floor(ue);
             fl[ax] = (T)fe;
@@ -312,6 +352,9 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
       v[12 + 6 * b] += k0z * rX[b].re + er2 * rXJ[b].re; v[13 + 6 * b] += k0z * rX[b].im + er2 * rXJ[b].im;
     }
   }
+  };
+  if (tmask) unit_loop(std::true_type{});
+  else unit_loop(std::false_type{});
 
   {
     const T* v = acc.v;
@@ -485,12 +528,13 @@ cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t s
     CascadeArgs c = a;
     c.pose_offset = a.pose_offset + p0;
     unsigned grid = (unsigned)(np * a.blocks_per_pose);
+    const size_t tsm = (a.precision == 32 ? sizeof(cx<float>) : sizeof(cx<double>)) * (a.w[0] + a.w[1] + a.w[2]);
     if (a.precision == 32) {
-      if (a.wrap) cascade3d_kernel<float, true><<<grid, kThreads, 0, st>>>(c);
-      else cascade3d_kernel<float, false><<<grid, kThreads, 0, st>>>(c);
+      if (a.wrap) cascade3d_kernel<float, true><<<grid, kThreads, tsm, st>>>(c);
+      else cascade3d_kernel<float, false><<<grid, kThreads, tsm, st>>>(c);
     } else {
-      if (a.wrap) cascade3d_kernel<double, true><<<grid, kThreads, 0, st>>>(c);
-      else cascade3d_kernel<double, false><<<grid, kThreads, 0, st>>>(c);
+      if (a.wrap) cascade3d_kernel<double, true><<<grid, kThreads, tsm, st>>>(c);
+      else cascade3d_kernel<double, false><<<grid, kThreads, tsm, st>>>(c);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

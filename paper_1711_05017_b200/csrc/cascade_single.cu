@@ -44,6 +44,7 @@ struct SinglePose {
   double kq[3][3];     // G_g += 2 pi i kq[g][a] Z_a     (= dw_a q_g[a])
   double kt[3];        // T_a  = 2 pi i kt[a] Z_a        (= dw_a)
   long long ufix[3][4];  // fixed-point u_a = ufix[a][3] + sum_b ufix[a][b] kappa_b
+  int tie_dep[3];  // column a of R has one nonzero, in row tie_dep[a] (else -1): see tie table
 };
 
 // Cluster stage state (shared memory of every CTA; used in rank 0): the
@@ -144,6 +145,14 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   // dynamic: transpose buffer tr[26][257] (reduction) | px | py | pz
   T(*tr)[kTrLd] = reinterpret_cast<T(*)[kTrLd]>(smem_raw);
   cx<T>* ptab = reinterpret_cast<cx<T>*>(smem_raw + sizeof(T) * kNumMoments * kTrLd + 16);
+  // tie table: for an axis a whose R column has a single nonzero (row b --
+  // lattice-aligned poses: identity, screws about a grid axis) the reference
+  // index u_a depends on k_b alone, and on such poses EVERY mode sits on an
+  // integer u_a.  Its float64 reference floor and fraction are tabulated
+  // once per pose at [offset(b) + k_b] (distinct b per a: R is a rotation)
+  // as (floor, frac) in T, so the tie branch is one shared load instead of a
+  // float64 divide and three float64 conversions per mode.
+  cx<T>* ttab = ptab + (a.w[0] + a.w[1] + a.w[2]);
 
   const int tid = threadIdx.x;
   unsigned long long* dbg = a.debug ? a.debug + (int64_t)blockIdx.x * 8 : nullptr;
@@ -204,11 +213,28 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     sp.nP = ((sp.p == 0 ? w0 : (sp.p == 1 ? w1 : w2)) + 15) / 16;
     sp.nQ = ((sp.q == 0 ? w0 : (sp.q == 1 ? w1 : w2)) + 15) / 16;
   }
-  // per-axis translation phase tables, concurrently with the sections above
+  if (tid == 192) {
+    for (int ax = 0; ax < 3; ++ax) {
+      const int nz = (src[ax] != 0.0) + (src[3 + ax] != 0.0) + (src[6 + ax] != 0.0);
+      sp.tie_dep[ax] = nz != 1 ? -1 : (src[ax] != 0.0 ? 0 : (src[3 + ax] != 0.0 ? 1 : 2));
+    }
+  }
+  // per-axis translation phase tables (and tie tables), concurrently with the sections above
   for (int i = tid; i < w0 + w1 + w2; i += kThreads) {
     int ax = i < w0 ? 0 : (i < w0 + w1 ? 1 : 2);
     int k = i - (ax == 0 ? 0 : (ax == 1 ? w0 : w0 + w1));
     int hh = ax == 0 ? hx : (ax == 1 ? hy : hz);
+    // tie table entry: the axis c whose R column has its single nonzero in row ax
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const bool only = src[3 * ax + c] != 0.0 && src[3 * ((ax + 1) % 3) + c] == 0.0 && src[3 * ((ax + 2) % 3) + c] == 0.0;
+      if (only) {
+        const double ue = exact_u_s(src, a.dom, c, ax == 0 ? k : hx, ax == 1 ? k : hy, ax == 2 ? k : hz, hx, hy, hz,
+                                    c == 0 ? hx : (c == 1 ? hy : hz));
+        const double fe = floor(ue);
+        ttab[i] = mk<T>((T)fe, (T)(ue - fe));
+      }
+    }
     double cyc = (a.dom[ax] * src[9 + ax]) * (double)(k - hh);
     cyc -= rint(cyc);
     T sn, cs;
@@ -256,6 +282,8 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     fyr = r == 0 ? sp.ufix[1][0] : (r == 1 ? sp.ufix[1][1] : sp.ufix[1][2]);
     fzr = r == 0 ? sp.ufix[2][0] : (r == 1 ? sp.ufix[2][1] : sp.ufix[2][2]);
   }
+  // axes read from the tie table (uniform over the block)
+  const int tmask = (sp.tie_dep[0] >= 0 ? 1 : 0) | (sp.tie_dep[1] >= 0 ? 2 : 0) | (a.dim == 3 && sp.tie_dep[2] >= 0 ? 4 : 0);
   long long fu3[3] = {0, 0, 0};
   cx<T> ph_pq = mk<T>(1, 0);
   int prev_run = -1, prev_kr = -2;
@@ -295,6 +323,17 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
         fl[ax] = (T)fix_floor(fu3[ax]);
         f[ax] = fix_frac(lo[ax]);
       }
+      if (tmask) {  // lattice-aligned axes: the tabulated reference floor / frac, never a tie
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+          if ((tmask >> ax) & 1) {
+            const int dep = sp.tie_dep[ax];
+            const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
+            fl[ax] = e.re;
+            f[ax] = e.im;
+            lo[ax] = 0x80000000u;
+          }
+      }
       const bool tz = a.dim == 3 && fix_tie(lo[2]);
       if (fix_tie(lo[0]) || fix_tie(lo[1]) || tz) {
 #pragma unroll
@@ -311,16 +350,27 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
       T u[3] = {fma(m02, kapz, fma(m01, kapy, fma(m00, kapx, (T)hx))),
                 fma(m12, kapz, fma(m11, kapy, fma(m10, kapx, (T)hy))),
                 fma(m22, kapz, fma(m21, kapy, fma(m20, kapx, (T)hz)))};
+      bool tie[3];
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         fl[ax] = floor(u[ax]);
         f[ax] = u[ax] - fl[ax];
+        tie[ax] = !((tmask >> ax) & 1) && (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
       }
-      const bool tz = a.dim == 3 && (f[2] < eps || f[2] > (T)1 - eps);
-      if (f[0] < eps || f[0] > (T)1 - eps || f[1] < eps || f[1] > (T)1 - eps || tz) {
+      if (tmask) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax)
+          if ((tmask >> ax) & 1) {
+            const int dep = sp.tie_dep[ax];
+            const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
+            fl[ax] = e.re;
+            f[ax] = e.im;
+          }
+      }
+      if (tie[0] || tie[1] || tie[2]) {
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-          if ((ax < 2 || tz) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
+          if (tie[ax]) {
             double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
             double fe = floor(ue);
             fl[ax] = (T)fe;
@@ -582,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_
 
 template <typename T, bool WRAP>
 cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
-  size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
+  size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + 2 * sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
   static size_t configured = 0;
   if (smem > configured && smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(cascade3d_single_kernel<T, WRAP>,
@@ -630,7 +680,7 @@ int single_blocks(const CascadeArgs& a, int sms) {
 
 template <typename T, bool WRAP>
 cudaError_t launch_server_t(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st) {
-  size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
+  size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + 2 * sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(cascade3d_server_kernel<T, WRAP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -48,6 +48,7 @@ struct RotArgs {
   double mu[3][3];       // u_a = h_a + sum_b mu[a][b] kappa_b
   long long ufix[3][3];  // to_fix32(mu)
   int perm[3];           // brick lane order: fastest, middle, slowest mode axis
+  int tie_dep[3];        // column a of R has one nonzero, in row tie_dep[a] (else -1)
 };
 
 __device__ __forceinline__ double exact_u_f(const double* R, const double* dom, int a, int kx, int ky, int kz, int hx,
@@ -57,80 +58,6 @@ __device__ __forceinline__ double exact_u_f(const double* R, const double* dom, 
   double oz = __dmul_rn((double)(kz - hz), dom[2]);
   double s = __dadd_rn(__dadd_rn(__dmul_rn(R[0 + a], ox), __dmul_rn(R[3 + a], oy)), __dmul_rn(R[6 + a], oz));
   return __dadd_rn(__ddiv_rn(-s, dom[a]), (double)ha);
-}
-
-template <typename T, bool WRAP>
-__global__ void __launch_bounds__(256) rotate_product_kernel(RotArgs a) {
-  using P4 = typename pair4<T>::type;
-  const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
-  const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
-  const int64_t n = (int64_t)a.nkx * w1 * w2;
-  const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
-  const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
-  const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
-  cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
-  // mu[a][b] = -R[b][a] dw_b / dw_a
-  double mu[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) mu[i][j] = -a.R[j * 3 + i] * (a.dom[j] / a.dom[i]);
-  const T eps = (T)a.tie_eps;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int kz = (int)(e % w2);
-    const int64_t r = e / w2;
-    const int ky = (int)(r % w1), kx = a.kx0 + (int)(r / w1);
-    const double kap[3] = {(double)(kx - hx), (double)(ky - hy), (double)(kz - hz)};
-    T fl[3], f[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      double h = ax == 0 ? hx : (ax == 1 ? hy : hz);
-      T u = (T)(h + mu[ax][0] * kap[0] + mu[ax][1] * kap[1] + mu[ax][2] * kap[2]);
-      fl[ax] = floor(u);
-      f[ax] = u - fl[ax];
-      const bool tie = (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
-      if (tie) {
-        double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
-        double fe = floor(ue);
-        fl[ax] = (T)fe;
-        f[ax] = (T)(ue - fe);
-      }
-    }
-    int ix = (int)fl[0], iy = (int)fl[1], iz = (int)fl[2];
-    cx<T> V = mk<T>(0, 0);
-    bool live = true;
-    if (WRAP) {
-      ix = ((ix % w0) + w0) % w0;
-      iy = ((iy % w1) + w1) % w1;
-      iz = ((iz % w2) + w2) % w2;
-    } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
-               (unsigned)(iz + 1) > (unsigned)w2) {
-      live = false;
-    }
-    if (live) {
-      const P4* p = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
-      P4 e00 = ldg_pair(p), e10 = ldg_pair(p + sx), e01 = ldg_pair(p + sy), e11 = ldg_pair(p + sx + sy);
-      const T fu = f[0], fv = f[1], fs = f[2];
-      cx<T> a00 = lerp(mk<T>(e00.x, e00.y), mk<T>(e10.x, e10.y), fu);
-      cx<T> a01 = lerp(mk<T>(e00.z, e00.w), mk<T>(e10.z, e10.w), fu);
-      cx<T> a10 = lerp(mk<T>(e01.x, e01.y), mk<T>(e11.x, e11.y), fu);
-      cx<T> a11 = lerp(mk<T>(e01.z, e01.w), mk<T>(e11.z, e11.w), fu);
-      V = lerp(lerp(a00, a10, fv), lerp(a01, a11, fv), fs);
-    }
-    // separable phase exp(2 pi i sum_a kappa_a dw_a s_a), reduced in float64
-    double cyc = 0.0;
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      double c = a.dom[ax] * a.s[ax] * kap[ax];
-      cyc += c - rint(c);
-    }
-    cyc -= rint(cyc);
-    double sn, cs;
-    sincospi(2.0 * cyc, &sn, &cs);
-    cx<T> q = V * mk<T>((T)cs, (T)sn);
-    if (C1) q = C1[((int64_t)kx * w1 + ky) * w2 + kz] * q;
-    out[e] = q;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -317,6 +244,7 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
   using P4 = typename pair4<T>::type;
   __shared__ cx<T> sq[8 * 73];
   __shared__ cx<T> ph[3][8];  // exp(2 pi i dw_a s_a (k_a - h_a)) for this brick's 8 modes per axis
+  __shared__ cx<T> tt[3][8];  // lattice-aligned poses: (floor, frac) of u_c at this brick's k_b, b = tie_dep[c]
   const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
   const int nbz = (w2 + 7) / 8, nby = (w1 + 7) / 8;
@@ -337,6 +265,17 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
     double sn, cs;
     sincospi(2.0 * cyc, &sn, &cs);
     ph[ax][o] = mk<T>((T)cs, (T)sn);
+  } else if (t >= 32 && t < 56) {  // tie table: row b, brick offset o
+    const int b = (t - 32) >> 3, o = t & 7;
+    const int k = b == 0 ? a.kx0 + bx * 8 + o : (b == 1 ? by * 8 + o : bz * 8 + o);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (a.tie_dep[c] != b) continue;
+      const double ue = exact_u_f(a.R, a.dom, c, b == 0 ? k : hx, b == 1 ? k : hy, b == 2 ? k : hz, hx, hy, hz,
+                                  c == 0 ? hx : (c == 1 ? hy : hz));
+      const double fe = floor(ue);
+      tt[b][o] = mk<T>((T)fe, (T)(ue - fe));
+    }
   }
   __syncthreads();
   // C1 for the epilogue's (z-fastest) modes, issued before the gathers
@@ -372,7 +311,13 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
       }
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
-        if ((ax < 2 || a.dim == 3) && fix_tie(lo[ax])) {
+        if (!(ax < 2 || a.dim == 3)) continue;
+        const int dep = a.tie_dep[ax];
+        if (dep >= 0) {  // lattice-aligned axis: tabulated reference floor / frac
+          const cx<T> e = tt[dep][dep == 0 ? ox : (dep == 1 ? oy : oz)];
+          fl[ax] = e.re;
+          f[ax] = e.im;
+        } else if (fix_tie(lo[ax])) {
           double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
           double fe = floor(ue);
           fl[ax] = (T)fe;
@@ -386,7 +331,13 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
         double u = h0 + a.mu[ax][0] * kk[0] + a.mu[ax][1] * kk[1] + a.mu[ax][2] * kk[2];
         fl[ax] = floor(u);
         f[ax] = u - fl[ax];
-        if ((ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps)) {
+        if (!(ax < 2 || a.dim == 3)) continue;
+        const int dep = a.tie_dep[ax];
+        if (dep >= 0) {
+          const cx<T> e = tt[dep][dep == 0 ? ox : (dep == 1 ? oy : oz)];
+          fl[ax] = e.re;
+          f[ax] = e.im;
+        } else if (f[ax] < eps || f[ax] > (T)1 - eps) {
           double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, (int)h0);
           double fe = floor(ue);
           fl[ax] = fe;
@@ -475,6 +426,10 @@ int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double* d
       a.mu[i][jj] = -a.R[jj * 3 + i] * (a.dom[jj] / a.dom[i]);
       a.ufix[i][jj] = to_fix32(a.mu[i][jj]);
     }
+  for (int c = 0; c < 3; ++c) {
+    const int nz = (a.R[c] != 0.0) + (a.R[3 + c] != 0.0) + (a.R[6 + c] != 0.0);
+    a.tie_dep[c] = nz != 1 ? -1 : (a.R[c] != 0.0 ? 0 : (a.R[3 + c] != 0.0 ? 1 : 2));
+  }
   // lane order: fastest along the mode axis whose u-step is most aligned with
   // C2's contiguous (z) axis, then the one most aligned with y
   {

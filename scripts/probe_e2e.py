@@ -59,3 +59,53 @@ with be.HapticServer(W1, W2, False, dom, 1.0, cen) as srv:
         q.arg[:9] = Rs[i].ravel(); q.arg[9:12] = ts[i]
         t0 = time.perf_counter(); fq(srv.id, q.pR, q.pt, q.pout); lat.append((time.perf_counter() - t0) * 1e6)
     print("F server raw query        ", pct(lat))
+# G: the C5-style call chain -- evaluate() in a haptic_session on stub assets
+from paper_1711_05017_b200.descriptor import SampleGrid
+from paper_1711_05017_b200.energy import Configuration, evaluate, haptic_session
+N = 2 * w
+g = SampleGrid(3, (N,) * 3, (-2.0,) * 3, 4.0 / N)
+
+
+class _A:
+    def __init__(s, win): s.grid, s.win, s.vector = g, win, None
+    def window(s, m=None): return s.win, False
+    def max_modes(s): return w ** 3
+
+
+a1, a2 = _A(W1), _A(W2)
+cfgs = [Configuration(Rs[i], ts[i]) for i in range(n)]
+with haptic_session(a1, a2):
+    for i in range(200): evaluate(a1, a2, cfgs[i])
+    lat = []
+    for i in range(n):
+        t0 = time.perf_counter(); evaluate(a1, a2, cfgs[i]); lat.append((time.perf_counter() - t0) * 1e6)
+    print("G session evaluate()      ", pct(lat))
+    lat = []
+    for i in range(n):
+        t0 = time.perf_counter(); evaluate(a1, a2, Configuration(Rs[i], ts[i])); lat.append((time.perf_counter() - t0) * 1e6)
+    print("H + Configuration()       ", pct(lat))
+    # I: the same call paced at a fixed period (busy wait between frames)
+    for period_us in (100.0, 1000.0):
+        lat = []
+        t_next = time.perf_counter()
+        for i in range(1000):
+            t0 = time.perf_counter(); evaluate(a1, a2, cfgs[i]); lat.append((time.perf_counter() - t0) * 1e6)
+            t_next += period_us * 1e-6
+            while time.perf_counter() < t_next:
+                pass
+        print(f"I paced every {period_us:6.0f} us   ", pct(lat))
+    # K: rotations about z (the C5 screw): mode z maps onto C2 z exactly -> index ties on every mode
+    def zrot(a):
+        c, s_ = np.cos(a), np.sin(a)
+        return np.array([[c, -s_, 0.0], [s_, c, 0.0], [0.0, 0.0, 1.0]])
+    zc = [Configuration(zrot(a), np.array([0.0, 0.0, 0.3 - 0.1 * a / (2 * np.pi)])) for a in np.linspace(0, 4 * np.pi, n)]
+    for i in range(200): evaluate(a1, a2, zc[i])
+    lat = []
+    for i in range(n):
+        t0 = time.perf_counter(); evaluate(a1, a2, zc[i]); lat.append((time.perf_counter() - t0) * 1e6)
+    print("K evaluate, z-axis screw  ", pct(lat))
+    ic = [Configuration(np.eye(3), ts[i]) for i in range(n)]
+    lat = []
+    for i in range(n):
+        t0 = time.perf_counter(); evaluate(a1, a2, ic[i]); lat.append((time.perf_counter() - t0) * 1e6)
+    print("L evaluate, identity R    ", pct(lat))
