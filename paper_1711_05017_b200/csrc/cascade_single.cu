@@ -94,6 +94,13 @@ __device__ __forceinline__ double exact_u_s(const double* R, const double* dom, 
   return __dadd_rn(__ddiv_rn(-s, dom[a]), (double)ha);
 }
 
+// tie-table floor stored in the real slot: as raw int bits for fp32 (no
+// int<->float conversion in the mode loop), as a value for fp64
+__device__ __forceinline__ float pack_floor(int v, float) { return __int_as_float(v); }
+__device__ __forceinline__ double pack_floor(int v, double) { return (double)v; }
+__device__ __forceinline__ int unpack_floor(float v) { return __float_as_int(v); }
+__device__ __forceinline__ int unpack_floor(double v) { return (int)v; }
+
 // Output slot i (0..13, interleaved complex) as a linear form of the 26
 // moments, from the coefficients precomputed in setup (14 threads).
 __device__ __forceinline__ double finalize_slot(const CascadeArgs& a, const SinglePose& sp, const double* m, int i) {
@@ -232,7 +239,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
         const double ue = exact_u_s(src, a.dom, c, ax == 0 ? k : hx, ax == 1 ? k : hy, ax == 2 ? k : hz, hx, hy, hz,
                                     c == 0 ? hx : (c == 1 ? hy : hz));
         const double fe = floor(ue);
-        ttab[i] = mk<T>((T)fe, (T)(ue - fe));
+        ttab[i] = mk<T>(pack_floor((int)fe, T(0)), (T)(ue - fe));
       }
     }
     double cyc = (a.dom[ax] * src[9 + ax]) * (double)(k - hh);
@@ -287,22 +294,50 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   long long fu3[3] = {0, 0, 0};
   cx<T> ph_pq = mk<T>(1, 0);
   int prev_run = -1, prev_kr = -2;
+  // unit -> (run, kr) advanced incrementally (no integer division per mode);
+  // the patch position (kp, kq) is recomputed only when the run changes
+  int kr = u_begin % wr, run = u_begin / wr;
+  int cached_run = -1, kp = 0, kq = 0;
+  bool pq_live = false;
+  const T er0 = r == 0 ? (T)1 : (T)0, er1 = r == 1 ? (T)1 : (T)0, er2 = r == 2 ? (T)1 : (T)0;
+  T kapx = (T)0, kapy = (T)0, kapz = (T)0;
   for (int unit = u_begin; unit < u_end; unit += u_step) {
-    const int kr = unit % wr;
-    const int run = unit / wr;
-    const int iq = run % sp.nQ;
-    const int ip = run / sp.nQ;
-    const int kp = 16 * ip + dp, kq = 16 * iq + dq;
-    if (kp >= wp || kq >= wq) continue;
+    if (unit != u_begin) {
+      if (u_step == 1) {
+        if (++kr == wr) {
+          kr = 0;
+          ++run;
+        }
+      } else {
+        kr = unit % wr;
+        run = unit / wr;
+      }
+    }
+    if (run != cached_run) {
+      cached_run = run;
+      kp = 16 * (run / sp.nQ) + dp;
+      kq = 16 * (run % sp.nQ) + dq;
+      pq_live = kp < wp && kq < wq;
+    }
+    if (!pq_live) continue;
     const int kx = p == 0 ? kp : (q == 0 ? kq : kr);
     const int ky = p == 1 ? kp : (q == 1 ? kq : kr);
     const int kz = p == 2 ? kp : (q == 2 ? kq : kr);
-    const T kapx = (T)(kx - hx), kapy = (T)(ky - hy), kapz = (T)(kz - hz);
     const bool step = run == prev_run && kr == prev_kr + 1;
-    if (!step) ph_pq = pt_p[kp] * pt_q[kq];
+    if (step) {  // one exact float add instead of three int->float conversions
+      kapx += er0;
+      kapy += er1;
+      kapz += er2;
+    } else {
+      kapx = (T)(kx - hx);
+      kapy = (T)(ky - hy);
+      kapz = (T)(kz - hz);
+      ph_pq = pt_p[kp] * pt_q[kq];
+    }
     prev_run = run;
     prev_kr = kr;
-    T fl[3], f[3];
+    int il[3];
+    T f[3];
     if constexpr (sizeof(T) == 4) {
       // exact 32.32 fixed-point index; float64 reference order only within 1e-6 of an integer
       if (step) {
@@ -320,7 +355,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         lo[ax] = fix_lo(fu3[ax]);
-        fl[ax] = (T)fix_floor(fu3[ax]);
+        il[ax] = fix_floor(fu3[ax]);
         f[ax] = fix_frac(lo[ax]);
       }
       if (tmask) {  // lattice-aligned axes: the tabulated reference floor / frac, never a tie
@@ -329,7 +364,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
           if ((tmask >> ax) & 1) {
             const int dep = sp.tie_dep[ax];
             const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
-            fl[ax] = e.re;
+            il[ax] = unpack_floor(e.re);
             f[ax] = e.im;
             lo[ax] = 0x80000000u;
           }
@@ -341,7 +376,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
           if ((ax < 2 || tz) && fix_tie(lo[ax])) {
             double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
             double fe = floor(ue);
-            fl[ax] = (T)fe;
+            il[ax] = (int)fe;
             f[ax] = (T)(ue - fe);
           }
         }
@@ -353,8 +388,9 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
       bool tie[3];
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
-        fl[ax] = floor(u[ax]);
-        f[ax] = u[ax] - fl[ax];
+        const T fl = floor(u[ax]);
+        il[ax] = (int)fl;
+        f[ax] = u[ax] - fl;
         tie[ax] = !((tmask >> ax) & 1) && (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
       }
       if (tmask) {
@@ -363,7 +399,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
           if ((tmask >> ax) & 1) {
             const int dep = sp.tie_dep[ax];
             const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
-            fl[ax] = e.re;
+            il[ax] = unpack_floor(e.re);
             f[ax] = e.im;
           }
       }
@@ -373,13 +409,13 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
           if (tie[ax]) {
             double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
             double fe = floor(ue);
-            fl[ax] = (T)fe;
+            il[ax] = (int)fe;
             f[ax] = (T)(ue - fe);
           }
         }
       }
     }
-    int ix = (int)fl[0], iy = (int)fl[1], iz = (int)fl[2];
+    int ix = il[0], iy = il[1], iz = il[2];
     if (WRAP) {
       ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
       iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
