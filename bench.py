@@ -68,6 +68,9 @@ def grid_params():
     center = np.full(3, origin + h * (GRID_N // 2))
     dom = np.full(3, 1.0 / (GRID_N * h))
     dcell = 1.0 / (GRID_N ** 3 * h ** 3)
+    # per-grid immutables, as energy._grid_constants hands them to every query
+    center.flags.writeable = False
+    dom.flags.writeable = False
     return h, center, dom, dcell
 
 

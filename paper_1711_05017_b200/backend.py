@@ -163,9 +163,16 @@ class _QueryBuffers(threading.local):
         self.pR, self.pt, self.pc, self.pd = (ctypes.c_void_p(a), ctypes.c_void_p(a + 72),
                                               ctypes.c_void_p(a + 96), ctypes.c_void_p(a + 120))
         self.pout = ctypes.c_void_p(self.out.ctypes.data)
+        # views used by the session path: one broadcast copy per operand
+        self.R33, self.t3 = self.arg[:9].reshape(3, 3), self.arg[9:12]
+        self.res3, self.res2 = self.out[:14].view(np.complex128), self.out[:8].view(np.complex128)
 
 
 _qb = _QueryBuffers()
+
+
+def _immutable(x):
+    return type(x) is tuple or (type(x) is np.ndarray and not x.flags.writeable)
 
 
 def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
@@ -178,6 +185,18 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
     W2 = C2 if type(C2) is DeviceWindow else as_device_window(C2)
     d = W1.ndim
     q = _qb
+    bits = 64 if (precision or _precision) == "fp64" else 32
+    if _servers and d == 3:
+        # session path: only the pose travels (the server holds centre and
+        # domega); the per-call work is two buffer copies and one C call
+        srv = _servers.get((W1.handle, W2.handle, bool(wrap), bits))
+        if srv is not None and srv.dcell == dcell and srv.matches(center, domega):
+            q.R33[...] = R
+            q.t3[...] = t_eff
+            rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
+            if rc:
+                check(rc)
+            return q.res3.copy()
     arg = q.arg
     if d == 3:
         arg[:9] = R.ravel() if type(R) is np.ndarray else np.asarray(R, dtype=np.float64).ravel()
@@ -190,7 +209,6 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
         arg[12:14] = center
         arg[15:17] = domega
         arg[14] = arg[17] = 0.0
-    bits = 64 if (precision or _precision) == "fp64" else 32
     srv = _servers.get((W1.handle, W2.handle, bool(wrap), bits)) if _servers else None
     if srv is not None and srv.dcell == dcell and arg[12:18].tobytes() == srv.cd_bytes:
         rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
@@ -239,10 +257,24 @@ class HapticServer:
         cd = np.zeros(6)  # center (3) | domega (3), as laid out in the query buffer
         cd[:d], cd[3:3 + d] = self.center, self.dom
         self.cd_bytes = cd.tobytes()
+        self._c_ref = self._d_ref = None
         _servers[self.key] = self
 
-    def matches(self, dcell, dom, center):
-        return dcell == self.dcell and np.array_equal(dom, self.dom) and np.array_equal(center, self.center)
+    def matches(self, center, domega):
+        """True when (center, domega) are the server's grid constants.  The
+        same immutable objects (a tuple, a read-only array -- what
+        energy._grid_constants hands out) are recognised by identity after
+        the first byte-exact comparison."""
+        if center is self._c_ref and domega is self._d_ref:
+            return True
+        d = self.W1.ndim
+        cd = np.zeros(6)
+        cd[:d], cd[3:3 + d] = center, domega
+        if cd.tobytes() != self.cd_bytes:
+            return False
+        if _immutable(center) and _immutable(domega):
+            self._c_ref, self._d_ref = center, domega
+        return True
 
     def stop(self):
         if self.id:
