@@ -62,15 +62,15 @@ def synthetic_windows(w, seed=SEED):
     return C1, C2
 
 
-def grid_params():
+def grid_params(frozen=False):
     h = DOMAIN / GRID_N
     origin = -0.5 * DOMAIN
     center = np.full(3, origin + h * (GRID_N // 2))
     dom = np.full(3, 1.0 / (GRID_N * h))
     dcell = 1.0 / (GRID_N ** 3 * h ** 3)
-    # per-grid immutables, as energy._grid_constants hands them to every query
-    center.flags.writeable = False
-    dom.flags.writeable = False
+    if frozen:  # per-grid immutables, as energy._grid_constants hands them to every query
+        center.flags.writeable = False
+        dom.flags.writeable = False
     return h, center, dom, dcell
 
 
@@ -300,7 +300,7 @@ def run_engine(args):
 
     _lib.ensure_device(local)
     prec = args.precision
-    h, center, dom, dcell = grid_params()
+    h, center, dom, dcell = grid_params(frozen=True)
     C1, C2 = synthetic_windows(W)
     W1, W2 = backend.DeviceWindow(C1), backend.DeviceWindow(C2)
     n_total = QUERIES_PER_STEP * (args.steps + args.warmup)
