@@ -1,20 +1,26 @@
-// cascade_single.cu -- latency kernel for ONE pose (the haptic query, Q1).
+// cascade_single.cu -- latency kernel for ONE pose (the haptic query, Q1),
+// one-shot or as a resident server.
 //
 // Same semantics as cascade.cu (reference _core.cascade_3d,
 // /root/reference/pkg/src/geofield/_core.pyx:598-724).  A lone query has
-// only ~10^5-10^6 modes, so latency is set by how many warps are resident
-// and how long each thread's dependency chain is, not by bandwidth:
-//   * every thread handles ~1-3 modes (no per-run setup): the translation
-//     phase comes from per-axis tables px/py/pz built once per CTA
-//     (sincospi of float64-reduced arguments), the continuous index from 9
-//     FMAs, so no thread waits on a long serial chain;
-//   * register cap 64 (4 CTAs of 256 threads per SM, 32 warps) so the grid
-//     is one resident wave of 4 x 148 CTAs that hides gather latency;
-//   * the 26 moments are reduced through a shared-memory transpose (fixed
-//     order) instead of 26 five-level shuffle trees, then across CTAs by a
-//     last-block-done pass in fixed block order (bitwise repeatable).
-// Lane layout: the same per-pose oriented 4 x 8 patches as cascade.cu, so
-// the corner gathers of a warp share few 128-byte lines.
+// only ~10^5-10^6 modes, so latency is set by the setup, the per-thread
+// dependency chain and the cross-CTA reduction tail, not by bandwidth:
+//   * setup: per-axis translation-phase tables (sincospi of float64-reduced
+//     arguments), 32.32 fixed-point index coefficients, the lane orientation
+//     and -- for lattice-aligned poses -- the tie tables, all from the pose
+//     in one pass and one barrier;
+//   * mode loop: 2 x 148 CTAs of 256 threads; each CTA walks a contiguous
+//     run of units (consecutive run-axis planes of one oriented 4 x 8 lane
+//     patch), so the fixed-point index advances by exact integer adds, the
+//     p/q phase product is reused and consecutive gathers reuse L1 lines;
+//   * reduction: 26 moments through a conflict-free shared-memory transpose,
+//     cluster ranks push their block moments to the cluster leader through
+//     DSMEM (mbarrier hand-off), leaders write partials, and the last leader
+//     (integer ticket) sums them in fixed order -- bitwise repeatable;
+//   * result: 28 self-tagged 8-byte words written to host-mapped memory, so
+//     the host needs no completion flag and the kernel no system fence.
+// The server variant keeps the grid resident (cooperative + clustered
+// launch); CTA 0 polls the host mailbox and forwards each pose through L2.
 #include "cascade.cuh"
 #include "common.cuh"
 
@@ -52,6 +58,11 @@ struct SinglePose {
 // and arrive on `bar` (release.cluster); rank 0 waits on it (acquire) -- a
 // one-way hand-off, no cluster-wide barrier on the query path.
 constexpr int kMaxCluster = 8;
+// resident CTAs per SM the register budget is sized for: the server grid is
+// 2 x 148 CTAs (up to 128 registers); the one-shot kernel keeps room for a
+// third so the next launch's CTAs can start beside the previous tail
+constexpr int kMinBlocksServer = 2;
+constexpr int kMinBlocksLaunch = 3;
 struct ClusterRed {
   double gather[kMaxCluster][kNumMoments];
   unsigned long long bar;
@@ -550,7 +561,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
 }
 
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_single_kernel(CascadeArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocksLaunch) cascade3d_single_kernel(CascadeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SinglePose sp;
   __shared__ double red[kNumMoments];
@@ -575,7 +586,7 @@ constexpr unsigned long long kServerStop = ~0ull;
 constexpr int kPollWarps = 2;  // CTA 0 warps polling the host mailbox
 
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 ? 3 : 2)) cascade3d_server_kernel(CascadeArgs a,
+__global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_kernel(CascadeArgs a,
                                                                                                ServerCtl ctl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SinglePose sp;
