@@ -62,7 +62,10 @@ constexpr int kMaxCluster = 8;
 // 2 x 148 CTAs (up to 128 registers); the one-shot kernel keeps room for a
 // third so the next launch's CTAs can start beside the previous tail
 constexpr int kMinBlocksServer = 2;
-constexpr int kMinBlocksLaunch = 3;
+#ifndef GF_LAUNCH_MINB
+#define GF_LAUNCH_MINB 3
+#endif
+constexpr int kMinBlocksLaunch = GF_LAUNCH_MINB;
 struct ClusterRed {
   double gather[kMaxCluster][kNumMoments];
   unsigned long long bar;
@@ -281,16 +284,15 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   Acc26<T> acc;
   acc.zero();
   GF_STAMP(1)
-  // each CTA takes a contiguous run of units: consecutive kr planes of one
-  // (p, q) patch, whose rotated C2 footprints overlap -> L1 reuse across the
-  // CTA's iterations (GF_SINGLE_ORDER=0: round-robin, for comparison)
+  // Each CTA takes a contiguous range of units; consecutive units are
+  // consecutive run-axis planes of one (p, q) patch, so the range splits into
+  // segments walked by the inner loop: the fixed-point index advances by one
+  // exact integer add per axis, C1 by one stride, and the seven per-mode
+  // products go into 8 run sums (sum Y, sum j Y) folded into the 26 moments
+  // once per segment -- the batched sweep's loop shape (cascade.cu).
   const int upb = (units + gridDim.x - 1) / gridDim.x;
-  const int u_begin = a.tile == 0 ? blockIdx.x * upb : blockIdx.x;
-  const int u_step = a.tile == 0 ? 1 : gridDim.x;
-  const int u_end = a.tile == 0 ? min(units, u_begin + upb) : units;
-  // Along a CTA's contiguous unit range consecutive units are consecutive
-  // run-axis planes of one (p, q) patch: the fixed-point index advances by
-  // one exact integer add per axis and the p/q phase product is reused.
+  const int u_begin = blockIdx.x * upb;
+  const int u_end = min(units, u_begin + upb);
   const cx<T>* pt_p = ptab + (p == 0 ? 0 : (p == 1 ? w0 : w0 + w1));
   const cx<T>* pt_q = ptab + (q == 0 ? 0 : (q == 1 ? w0 : w0 + w1));
   const cx<T>* pt_r = ptab + (r == 0 ? 0 : (r == 1 ? w0 : w0 + w1));
@@ -300,161 +302,161 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     fyr = r == 0 ? sp.ufix[1][0] : (r == 1 ? sp.ufix[1][1] : sp.ufix[1][2]);
     fzr = r == 0 ? sp.ufix[2][0] : (r == 1 ? sp.ufix[2][1] : sp.ufix[2][2]);
   }
+  const T mr0 = r == 0 ? m00 : (r == 1 ? m01 : m02);  // fp64 engine: du_a / dk_r
+  const T mr1 = r == 0 ? m10 : (r == 1 ? m11 : m12);
+  const T mr2 = r == 0 ? m20 : (r == 1 ? m21 : m22);
   // axes read from the tie table (uniform over the block)
   const int tmask = (sp.tie_dep[0] >= 0 ? 1 : 0) | (sp.tie_dep[1] >= 0 ? 2 : 0) | (a.dim == 3 && sp.tie_dep[2] >= 0 ? 4 : 0);
-  long long fu3[3] = {0, 0, 0};
-  cx<T> ph_pq = mk<T>(1, 0);
-  int prev_run = -1, prev_kr = -2;
-  // unit -> (run, kr) advanced incrementally (no integer division per mode);
-  // the patch position (kp, kq) is recomputed only when the run changes
-  int kr = u_begin % wr, run = u_begin / wr;
-  int cached_run = -1, kp = 0, kq = 0;
-  bool pq_live = false;
+  const int sr = r == 0 ? w1 * w2 : (r == 1 ? w2 : 1);  // C1 stride along the run axis
   const T er0 = r == 0 ? (T)1 : (T)0, er1 = r == 1 ? (T)1 : (T)0, er2 = r == 2 ? (T)1 : (T)0;
-  T kapx = (T)0, kapy = (T)0, kapz = (T)0;
-  for (int unit = u_begin; unit < u_end; unit += u_step) {
-    if (unit != u_begin) {
-      if (u_step == 1) {
-        if (++kr == wr) {
-          kr = 0;
-          ++run;
-        }
-      } else {
-        kr = unit % wr;
-        run = unit / wr;
-      }
-    }
-    if (run != cached_run) {
-      cached_run = run;
-      kp = 16 * (run / sp.nQ) + dp;
-      kq = 16 * (run % sp.nQ) + dq;
-      pq_live = kp < wp && kq < wq;
-    }
-    if (!pq_live) continue;
-    const int kx = p == 0 ? kp : (q == 0 ? kq : kr);
-    const int ky = p == 1 ? kp : (q == 1 ? kq : kr);
-    const int kz = p == 2 ? kp : (q == 2 ? kq : kr);
-    const bool step = run == prev_run && kr == prev_kr + 1;
-    if (step) {  // one exact float add instead of three int->float conversions
-      kapx += er0;
-      kapy += er1;
-      kapz += er2;
-    } else {
-      kapx = (T)(kx - hx);
-      kapy = (T)(ky - hy);
-      kapz = (T)(kz - hz);
-      ph_pq = pt_p[kp] * pt_q[kq];
-    }
-    prev_run = run;
-    prev_kr = kr;
-    int il[3];
-    T f[3];
+  for (int seg = u_begin; seg < u_end;) {
+    const int run = seg / wr, kr0 = seg % wr;
+    const int kend = min(wr, kr0 + (u_end - seg));
+    seg += kend - kr0;
+    const int kp = 16 * (run / sp.nQ) + dp, kq = 16 * (run % sp.nQ) + dq;
+    if (kp >= wp || kq >= wq) continue;
+    const int kx0 = p == 0 ? kp : (q == 0 ? kq : kr0);
+    const int ky0 = p == 1 ? kp : (q == 1 ? kq : kr0);
+    const int kz0 = p == 2 ? kp : (q == 2 ? kq : kr0);
+    const T k0x = (T)(kx0 - hx), k0y = (T)(ky0 - hy), k0z = (T)(kz0 - hz);
+    const cx<T> ph_pq = pt_p[kp] * pt_q[kq];
+    long long fu3[3] = {0, 0, 0};
+    T u0[3] = {(T)0, (T)0, (T)0};
     if constexpr (sizeof(T) == 4) {
-      // exact 32.32 fixed-point index; float64 reference order only within 1e-6 of an integer
-      if (step) {
+      const int kk[3] = {kx0 - hx, ky0 - hy, kz0 - hz};
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax)
+        fu3[ax] = sp.ufix[ax][3] + (long long)kk[0] * sp.ufix[ax][0] + (long long)kk[1] * sp.ufix[ax][1] +
+                  (long long)kk[2] * sp.ufix[ax][2];
+    } else {
+      u0[0] = fma(m02, k0z, fma(m01, k0y, fma(m00, k0x, (T)hx)));
+      u0[1] = fma(m12, k0z, fma(m11, k0y, fma(m10, k0x, (T)hy)));
+      u0[2] = fma(m22, k0z, fma(m21, k0y, fma(m20, k0x, (T)hz)));
+    }
+    cx<T> rS = mk<T>(0, 0), rJ = mk<T>(0, 0);
+    cx<T> rX[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
+    cx<T> rXJ[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
+    int c1off = (kx0 * w1 + ky0) * w2 + kz0;
+    for (int kr = kr0; kr < kend; ++kr, c1off += sr) {
+      const T j = (T)(kr - kr0);
+      int il[3];
+      T f[3];
+      if constexpr (sizeof(T) == 4) {
+        // exact 32.32 fixed-point index; float64 reference order only within 1e-6 of an integer
+        unsigned lo[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          lo[ax] = fix_lo(fu3[ax]);
+          il[ax] = fix_floor(fu3[ax]);
+          f[ax] = fix_frac(lo[ax]);
+        }
         fu3[0] += fxr;
         fu3[1] += fyr;
         fu3[2] += fzr;
+        if (tmask) {  // lattice-aligned axes: the tabulated reference floor / frac, never a tie
+          const int kx = r == 0 ? kr : kx0, ky = r == 1 ? kr : ky0, kz = r == 2 ? kr : kz0;
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax)
+            if ((tmask >> ax) & 1) {
+              const int dep = sp.tie_dep[ax];
+              const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
+              il[ax] = unpack_floor(e.re);
+              f[ax] = e.im;
+              lo[ax] = 0x80000000u;
+            }
+        }
+        const bool tz = a.dim == 3 && fix_tie(lo[2]);
+        if (fix_tie(lo[0]) || fix_tie(lo[1]) || tz) {
+          const int kx = r == 0 ? kr : kx0, ky = r == 1 ? kr : ky0, kz = r == 2 ? kr : kz0;
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            if ((ax < 2 || tz) && fix_tie(lo[ax])) {
+              double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+              double fe = floor(ue);
+              il[ax] = (int)fe;
+              f[ax] = (T)(ue - fe);
+            }
+          }
+        }
       } else {
-        const int kk[3] = {kx - hx, ky - hy, kz - hz};
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax)
-          fu3[ax] = sp.ufix[ax][3] + (long long)kk[0] * sp.ufix[ax][0] + (long long)kk[1] * sp.ufix[ax][1] +
-                    (long long)kk[2] * sp.ufix[ax][2];
-      }
-      unsigned lo[3];
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        lo[ax] = fix_lo(fu3[ax]);
-        il[ax] = fix_floor(fu3[ax]);
-        f[ax] = fix_frac(lo[ax]);
-      }
-      if (tmask) {  // lattice-aligned axes: the tabulated reference floor / frac, never a tie
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax)
-          if ((tmask >> ax) & 1) {
-            const int dep = sp.tie_dep[ax];
-            const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
-            il[ax] = unpack_floor(e.re);
-            f[ax] = e.im;
-            lo[ax] = 0x80000000u;
-          }
-      }
-      const bool tz = a.dim == 3 && fix_tie(lo[2]);
-      if (fix_tie(lo[0]) || fix_tie(lo[1]) || tz) {
+        const T u[3] = {fma(j, mr0, u0[0]), fma(j, mr1, u0[1]), fma(j, mr2, u0[2])};
+        bool tie[3];
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-          if ((ax < 2 || tz) && fix_tie(lo[ax])) {
-            double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
-            double fe = floor(ue);
-            il[ax] = (int)fe;
-            f[ax] = (T)(ue - fe);
+          const T fl = floor(u[ax]);
+          il[ax] = (int)fl;
+          f[ax] = u[ax] - fl;
+          tie[ax] = !((tmask >> ax) & 1) && (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
+        }
+        if (tmask || tie[0] || tie[1] || tie[2]) {
+          const int kx = r == 0 ? kr : kx0, ky = r == 1 ? kr : ky0, kz = r == 2 ? kr : kz0;
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            if ((tmask >> ax) & 1) {
+              const int dep = sp.tie_dep[ax];
+              const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
+              il[ax] = unpack_floor(e.re);
+              f[ax] = e.im;
+            } else if (tie[ax]) {
+              double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
+              double fe = floor(ue);
+              il[ax] = (int)fe;
+              f[ax] = (T)(ue - fe);
+            }
           }
         }
       }
-    } else {
-      T u[3] = {fma(m02, kapz, fma(m01, kapy, fma(m00, kapx, (T)hx))),
-                fma(m12, kapz, fma(m11, kapy, fma(m10, kapx, (T)hy))),
-                fma(m22, kapz, fma(m21, kapy, fma(m20, kapx, (T)hz)))};
-      bool tie[3];
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        const T fl = floor(u[ax]);
-        il[ax] = (int)fl;
-        f[ax] = u[ax] - fl;
-        tie[ax] = !((tmask >> ax) & 1) && (ax < 2 || a.dim == 3) && (f[ax] < eps || f[ax] > (T)1 - eps);
+      int ix = il[0], iy = il[1], iz = il[2];
+      if (WRAP) {
+        ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
+        iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
+        iz = iz < 0 ? iz + w2 : (iz >= w2 ? iz - w2 : iz);
+      } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
+                 (unsigned)(iz + 1) > (unsigned)w2) {
+        continue;  // whole footprint outside the window: exact zero contribution
       }
-      if (tmask) {
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax)
-          if ((tmask >> ax) & 1) {
-            const int dep = sp.tie_dep[ax];
-            const cx<T> e = ttab[dep == 0 ? kx : (dep == 1 ? w0 + ky : w0 + w1 + kz)];
-            il[ax] = unpack_floor(e.re);
-            f[ax] = e.im;
-          }
-      }
-      if (tie[0] || tie[1] || tie[2]) {
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          if (tie[ax]) {
-            double ue = exact_u_s(sp.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
-            double fe = floor(ue);
-            il[ax] = (int)fe;
-            f[ax] = (T)(ue - fe);
-          }
-        }
+      const P4* ptr = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
+      P4 e00 = ldg_pair(ptr), e10 = ldg_pair(ptr + sx), e01 = ldg_pair(ptr + sy), e11 = ldg_pair(ptr + sx + sy);
+      const cx<T> base = C1[c1off] * (ph_pq * pt_r[kr]);
+      const T fu = f[0], fv = f[1], fs = f[2];
+      cx<T> c000 = mk<T>(e00.x, e00.y), c001 = mk<T>(e00.z, e00.w);
+      cx<T> c100 = mk<T>(e10.x, e10.y), c101 = mk<T>(e10.z, e10.w);
+      cx<T> c010 = mk<T>(e01.x, e01.y), c011 = mk<T>(e01.z, e01.w);
+      cx<T> c110 = mk<T>(e11.x, e11.y), c111 = mk<T>(e11.z, e11.w);
+      cx<T> d00 = c100 - c000, d01 = c101 - c001, d10 = c110 - c010, d11 = c111 - c011;
+      cx<T> a00 = mk<T>(fma(fu, d00.re, c000.re), fma(fu, d00.im, c000.im));
+      cx<T> a01 = mk<T>(fma(fu, d01.re, c001.re), fma(fu, d01.im, c001.im));
+      cx<T> a10 = mk<T>(fma(fu, d10.re, c010.re), fma(fu, d10.im, c010.im));
+      cx<T> a11 = mk<T>(fma(fu, d11.re, c011.re), fma(fu, d11.im, c011.im));
+      cx<T> b0 = lerp(a00, a10, fv), b1 = lerp(a01, a11, fv);
+      cx<T> V = lerp(b0, b1, fs);
+      cx<T> dU = lerp(lerp(d00, d10, fv), lerp(d01, d11, fv), fs);
+      cx<T> dV = lerp(a10 - a00, a11 - a01, fs);
+      cx<T> dS = b1 - b0;
+      cx<T> bV = base * V;
+      cx<T> X0 = base * dU, X1 = base * dV, X2 = base * dS;
+      if constexpr (sizeof(T) == 4) {
+        rS += bV;
+        axpy(rJ, j, bV);
+        rX[0] += X0; rX[1] += X1; rX[2] += X2;
+        axpy(rXJ[0], j, X0); axpy(rXJ[1], j, X1); axpy(rXJ[2], j, X2);
+      } else {  // fp64 engine: straight into the moments (the run sums would spill)
+        acc.add(bV, X0, X1, X2, fma(j, er0, k0x), fma(j, er1, k0y), fma(j, er2, k0z));
       }
     }
-    int ix = il[0], iy = il[1], iz = il[2];
-    if (WRAP) {
-      ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
-      iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
-      iz = iz < 0 ? iz + w2 : (iz >= w2 ? iz - w2 : iz);
-    } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
-               (unsigned)(iz + 1) > (unsigned)w2) {
-      continue;
+    if constexpr (sizeof(T) == 8) continue;
+    // fold the segment: sum_j kappa_a(j) Y = kappa0_a sum Y + e_r,a sum j Y
+    T* v = acc.v;
+    v[0] += rS.re; v[1] += rS.im;
+    v[2] += k0x * rS.re + er0 * rJ.re; v[3] += k0x * rS.im + er0 * rJ.im;
+    v[4] += k0y * rS.re + er1 * rJ.re; v[5] += k0y * rS.im + er1 * rJ.im;
+    v[6] += k0z * rS.re + er2 * rJ.re; v[7] += k0z * rS.im + er2 * rJ.im;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      v[8 + 6 * b] += k0x * rX[b].re + er0 * rXJ[b].re;  v[9 + 6 * b] += k0x * rX[b].im + er0 * rXJ[b].im;
+      v[10 + 6 * b] += k0y * rX[b].re + er1 * rXJ[b].re; v[11 + 6 * b] += k0y * rX[b].im + er1 * rXJ[b].im;
+      v[12 + 6 * b] += k0z * rX[b].re + er2 * rXJ[b].re; v[13 + 6 * b] += k0z * rX[b].im + er2 * rXJ[b].im;
     }
-    const P4* ptr = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
-    P4 e00 = ldg_pair(ptr), e10 = ldg_pair(ptr + sx), e01 = ldg_pair(ptr + sy), e11 = ldg_pair(ptr + sx + sy);
-    const cx<T> base = C1[(kx * w1 + ky) * w2 + kz] * (ph_pq * pt_r[kr]);
-    const T fu = f[0], fv = f[1], fs = f[2];
-    cx<T> c000 = mk<T>(e00.x, e00.y), c001 = mk<T>(e00.z, e00.w);
-    cx<T> c100 = mk<T>(e10.x, e10.y), c101 = mk<T>(e10.z, e10.w);
-    cx<T> c010 = mk<T>(e01.x, e01.y), c011 = mk<T>(e01.z, e01.w);
-    cx<T> c110 = mk<T>(e11.x, e11.y), c111 = mk<T>(e11.z, e11.w);
-    cx<T> d00 = c100 - c000, d01 = c101 - c001, d10 = c110 - c010, d11 = c111 - c011;
-    cx<T> a00 = mk<T>(fma(fu, d00.re, c000.re), fma(fu, d00.im, c000.im));
-    cx<T> a01 = mk<T>(fma(fu, d01.re, c001.re), fma(fu, d01.im, c001.im));
-    cx<T> a10 = mk<T>(fma(fu, d10.re, c010.re), fma(fu, d10.im, c010.im));
-    cx<T> a11 = mk<T>(fma(fu, d11.re, c011.re), fma(fu, d11.im, c011.im));
-    cx<T> b0 = lerp(a00, a10, fv), b1 = lerp(a01, a11, fv);
-    cx<T> V = lerp(b0, b1, fs);
-    cx<T> dU = lerp(lerp(d00, d10, fv), lerp(d01, d11, fv), fs);
-    cx<T> dV = lerp(a10 - a00, a11 - a01, fs);
-    cx<T> dS = b1 - b0;
-    cx<T> bV = base * V;
-    acc.add(bV, base * dU, base * dV, base * dS, kapx, kapy, kapz);
   }
 
   GF_STAMP(2)
@@ -561,7 +563,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
 }
 
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(kThreads, kMinBlocksLaunch) cascade3d_single_kernel(CascadeArgs a) {
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? kMinBlocksLaunch : 2) cascade3d_single_kernel(CascadeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SinglePose sp;
   __shared__ double red[kNumMoments];
