@@ -163,3 +163,19 @@ def test_bench_pose_generator_is_cmd_bench_order():
     q = rng.normal(size=4)
     np.testing.assert_allclose(Rs[0], oracle.quat_rotation(q))
     np.testing.assert_allclose(ts[0], rng.uniform(-1.0, 1.0, 3))
+
+
+def test_haptic_realtime_enter_leave_restores_thread_state():
+    """HapticSession.run's servo-thread setup (pin + SCHED_FIFO) is undone on exit."""
+    import os
+
+    from paper_1711_05017_b200 import haptic
+
+    if not hasattr(os, "sched_setaffinity"):
+        pytest.skip("no sched_setaffinity")
+    aff, pol = os.sched_getaffinity(0), os.sched_getscheduler(0)
+    state = haptic._enter_realtime()
+    if state[2]:
+        assert len(os.sched_getaffinity(0)) == 1 and os.sched_getscheduler(0) == os.SCHED_FIFO
+    haptic._leave_realtime(state)
+    assert os.sched_getaffinity(0) == aff and os.sched_getscheduler(0) == pol
