@@ -40,7 +40,13 @@ def test_step_damped_matches_sequential_backtracking():
             want = sequential_step(a1, a2, 512, np.eye(3), t0, ev, 0.05, 1e-3, g.spacing)
             s.step_damped(ev)
             np.testing.assert_allclose(s.translation, want, rtol=0, atol=1e-15)
+        import os
+
+        aff, pol = os.sched_getaffinity(0), os.sched_getscheduler(0)
         stats = s.run([np.eye(3)] * 20, [t0] * 20, rate_hz=2000.0)
         assert stats["frames"] == 20 and stats["p99_us"] > 0
+        assert 0 <= stats["max_frame"] < 20 and isinstance(stats["realtime"], bool)
+        # the servo thread's affinity and scheduling policy are restored after the run
+        assert os.sched_getaffinity(0) == aff and os.sched_getscheduler(0) == pol
     finally:
         backend.set_precision("fp32")
