@@ -1,6 +1,7 @@
 """Multi-rank decomposition logic on CPU (gloo, world size 2).
 
-The pose sweep's sharding + gather and the landscape's plane -> slab
+The pose sweep's sharding + gather, the landscape's plane -> slab
+all-to-all and the node-sharded forward window's plane -> window-slab
 all-to-all run through the same host code the GPU path uses; the per-rank
 compute is the oracle (numpy / C restatement), so the test checks the
 decomposition, not the kernels (those are covered by the -m gpu suite).
@@ -61,6 +62,14 @@ def _centred_inverse(x, axis, n):
     return np.fft.ifft(full, axis=axis) * n
 
 
+def _centred_forward(x, axis, w):
+    """numpy: node-ordered input along axis -> the DC-centred w-mode window
+    of fftshift(fft(ifftshift(x))) (one pruned forward pass)."""
+    n = x.shape[axis]
+    y = np.fft.fftshift(np.fft.fft(np.fft.ifftshift(x, axes=axis), axis=axis), axes=axis)
+    return np.take(y, np.arange(n // 2 - w // 2, n // 2 + w // 2), axis=axis)
+
+
 def _worker(rank, world, port, results):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -95,6 +104,22 @@ def _worker(rank, world, port, results):
         full = oracle.score_field(C1, C2, False, N, origin, h, R)
         ylo, yhi = y_r[rank]
         results[f"field{rank}"] = float(np.max(np.abs(land - full[:, ylo:yhi])) / np.max(np.abs(full)))
+        # --- forward window of a node-sharded field: z, y passes on the
+        # rank's planes -> all-to-all -> x pass (parallel.forward_window_slab's plan)
+        rng = np.random.default_rng(7)
+        f = rng.normal(size=N) + 1j * rng.normal(size=N)
+        wn = 8
+        x_r = [parallel.shard_range(N[0], r, world) for r in range(world)]
+        wy_r = [parallel.shard_range(wn, r, world) for r in range(world)]
+        xlo, xhi = x_r[rank]
+        pz = _centred_forward(f[xlo:xhi], 2, wn)
+        py = _centred_forward(pz, 1, wn)
+        slab = parallel.exchange_planes_to_slabs(torch.view_as_real(torch.from_numpy(py)), x_r, wy_r, rank)
+        slab = torch.view_as_complex(slab.contiguous()).numpy()
+        win = _centred_forward(slab, 0, wn) * h ** 3
+        want = oracle.center_window(oracle.forward_dft(f, N, origin, h), N, origin, h, wn)
+        wlo, whi = wy_r[rank]
+        results[f"window{rank}"] = float(np.max(np.abs(win - want[:, wlo:whi])) / np.max(np.abs(want)))
         # --- density node slabs: halo planes make the neighbour fill exact
         g = SampleGrid(3, (8, 8, 8), (-0.8, -0.8, -0.8), 0.2)
         solid = scenes.box_mesh((0.2, 0.2, 0.2))
@@ -139,6 +164,7 @@ def test_sweep_and_slab_decomposition_gloo(world):
     for r in range(world):
         assert results[f"sweep{r}"] <= 1e-12
         assert results[f"field{r}"] <= 1e-12
+        assert results[f"window{r}"] <= 1e-12
         assert results[f"density{r}"]
 
 
