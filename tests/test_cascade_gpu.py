@@ -154,3 +154,32 @@ def test_haptic_server_2d_fp64_and_idle_timeout(be):
     with be.HapticServer(W1, W2, False, dom, 0.3, c, precision="fp64"):
         again = be.cascade(W1, W2, False, dom, 0.3, poses[0][0], poses[0][1], c, precision="fp64")
     np.testing.assert_array_equal(again, want[0])
+
+
+@pytest.mark.parametrize("w,wrap", [(48, False), (64, True), (96, False)])
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_cascade_3d_long_runs_launch_and_server(be, w, wrap, prec, tol):
+    """Windows large enough that every CTA walks several run-axis segments
+    (the segment loop's fold and its segment boundaries): launch path vs the
+    oracle, and the resident server vs the launch path (bit for bit in fp32)."""
+    rng = np.random.default_rng(5000 + w)
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom, dcell, c = (0.07, 0.07, 0.07), 0.21, rng.normal(size=3)
+    poses = [(random_rotation(rng), rng.uniform(-2, 2, 3)) for _ in range(2)]
+    got = [be.cascade(W1, W2, wrap, dom, dcell, R, t, c, precision=prec) for R, t in poses]
+    for g, (R, t) in zip(got, poses):
+        want = oracle.cascade(C1, C2, wrap, dom, dcell, R, t, c)
+        l1 = oracle.cascade_term_scales(C1, C2, wrap, dom, dcell, R, t, c)
+        assert np.all(parity_tol(g, want, l1, tol)), (g, want, l1)
+    with be.HapticServer(W1, W2, wrap, dom, dcell, c, precision=prec):
+        srv = [be.cascade(W1, W2, wrap, dom, dcell, R, t, c, precision=prec) for R, t in poses]
+    for s, g in zip(srv, got):
+        if prec == "fp32":
+            np.testing.assert_array_equal(s, g)
+        else:
+            # fp64 at w=96: the cooperative server grid may be refused its
+            # 4-CTA clusters (62 KB of shared memory per CTA) and fall back to
+            # a plain cooperative launch, whose cross-CTA sum has another
+            # association -- equal to the last bits, not bit for bit
+            np.testing.assert_allclose(s, g, rtol=0, atol=1e-14 * np.max(np.abs(g)))
