@@ -484,8 +484,7 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
   if (n_poses == 1 && a.variant == 1) {
     a.single = 1;
     a.blocks_per_pose = single_blocks(a, target_blocks / 2);
-    static const int order = getenv("GF_SINGLE_ORDER") ? atoi(getenv("GF_SINGLE_ORDER")) : 1;
-    a.tile = order ? 0 : 1;  // single kernel: 0 = contiguous unit runs per CTA, 1 = round-robin
+    a.tile = 0;  // single kernel: contiguous unit ranges per CTA (segment loop)
     return;
   }
   a.single = 0;
