@@ -7,7 +7,8 @@
  * backend.py:71-164 -> _core.pyx).  Plain pointers and sizes only; no torch
  * types.  Every function returns 0 on success, a cudaError_t (> 0) on a CUDA
  * failure, or a negative gf status (-1 bad argument, -2 out of host memory,
- * -3 internal); gf_last_error() then describes the failure (thread-local).
+ * -3 internal, -4 haptic server no longer running); gf_last_error() then
+ * describes the failure (thread-local).
  * Domain validation (rotation checks, grid mismatch, window budgets) stays in
  * the Python host layer with the reference's exception types.
  *
@@ -174,12 +175,6 @@ int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double *domega, 
 int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double *domega, const double *R,
                              const double *s, int precision, int kx0, int nkx, void *out_dev, void *stream);
 
-/* Fused landscape pass 1 for 3D windows: the product (as above, s given)
- * for window x-planes [kx0, kx0 + nkx) (nkx < 0: all), inverse-transformed
- * along z in registers: out (nkx, w1, n2), n2 in {32, ..., 512}. */
-int gf_field_zpass(uint64_t h1, uint64_t h2, int wrap, const double *domega, int n2, const double *R, const double *s,
-                   int precision, int kx0, int nkx, void *out_dev, void *stream);
-
 /* Full translational landscape (energy.score_field, energy.py:309-344):
  * the product above with s = Rc - c + origin, then three pruned inverse
  * passes to the dims grid, times scale (= 1 / (N^d dV)).  work_dev holds
@@ -204,21 +199,23 @@ int gf_measure_roundtrip(int n, double *out);
  * query per call through a host-mapped mailbox -- no kernel launch per
  * query.  Same window pair / grid for the server's lifetime; the kernel exits
  * after idle_timeout_s without requests (<= 0: 30 s) or on gf_server_stop.
- * gf_server_query has gf_cascade's pose and output conventions. */
+ * max_sms > 0 keeps the grid on about that many SMs (whole CTA clusters by
+ * SM id; the rest leave at start-up), so landscape exports and sweeps from
+ * other threads run beside a session; 0 uses every SM.
+ * gf_server_query has gf_cascade's pose and output conventions and returns
+ * -4 once the server has stopped or timed out (the caller falls back to
+ * gf_cascade). */
 int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double *domega, double dcell, const double *center,
-                    int precision, double idle_timeout_s, uint64_t *server_id);
+                    int precision, double idle_timeout_s, int max_sms, uint64_t *server_id);
 int gf_server_query(uint64_t server_id, const double *R, const double *t_eff, double *out);
 int gf_server_stop(uint64_t server_id);
 
-/* Tuning knobs for experiments: kernel variant (1 = direct gather, the
- * default; 0 = u-space tiled), the tiled variant's tile side, and the direct
- * variant's run length along the run axis per thread (0 = auto). */
-int gf_set_cascade_variant(int variant);
-int gf_set_cascade_tile(int tile);
-/* Debug: per-CTA phase timestamps (globaltimer ns) of the single-query kernel
- * into a device buffer of >= 8 x blocks uint64 (NULL disables). */
-int gf_set_cascade_debug(void *dev_buf);
+/* Experiment knobs: the batched sweep's run length along the run axis per
+ * thread (0 = auto), and per-CTA phase timestamps (globaltimer ns) of the
+ * single-query kernel into a device buffer of >= 8 x blocks uint64 (NULL
+ * disables). */
 int gf_set_cascade_run_length(int L);
+int gf_set_cascade_debug(void *dev_buf);
 
 #ifdef __cplusplus
 }

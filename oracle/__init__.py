@@ -113,12 +113,32 @@ def _elements(elems):
     raise ValueError("elements must be triangles (n, 9) or segments (n, 4)")
 
 
+def _rows(m, fn, min_rows=256):
+    """Run fn(i0, i1) over [0, m) in row blocks on every host core (the C
+    kernels release nothing shared; ctypes drops the GIL).  Per-point
+    results do not depend on the split."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    nt = max(1, min(os.cpu_count() or 1, m // min_rows))
+    if nt == 1:
+        fn(0, m)
+        return
+    bounds = np.linspace(0, m, 4 * nt + 1).astype(np.int64)
+    with ThreadPoolExecutor(max_workers=nt) as pool:
+        list(pool.map(lambda k: fn(int(bounds[k]), int(bounds[k + 1])), range(len(bounds) - 1)))
+
+
+def _at(a, i0):
+    """ctypes pointer to row i0 of a C-contiguous float64 / int64 array."""
+    return ctypes.cast(a.ctypes.data + i0 * a.strides[0], _ip if a.dtype == np.int64 else _dp)
+
+
 def distance(elems, P):
     """Exact min point-element distance (triangles (n,3,3) or segments (n,2,2))."""
     e, d = _elements(elems)
     P = _f64(P)
     out = np.empty(len(P))
-    lib().orc_distance_brute(d, _d(e), len(e), _d(P), len(P), _d(out))
+    _rows(len(P), lambda i0, i1: lib().orc_distance_brute(d, _d(e), len(e), _at(P, i0), i1 - i0, _at(out, i0)))
     return out
 
 
@@ -138,7 +158,7 @@ def winding(elems, P):
     e, d = _elements(elems)
     P = _f64(P)
     out = np.empty(len(P))
-    lib().orc_winding(d, _d(e), len(e), _d(P), len(P), _d(out))
+    _rows(len(P), lambda i0, i1: lib().orc_winding(d, _d(e), len(e), _at(P, i0), i1 - i0, _at(out, i0)))
     return out
 
 
@@ -151,8 +171,10 @@ def sweep(elems, normals, measures, P, xi_eff, sigma, gconst, max_angle, max_dep
     resid = np.zeros(len(P))
     clamps = np.zeros(len(P), dtype=np.int64)
     fn = lib().orc_sweep_3d if d == 3 else lib().orc_sweep_2d
-    fn(_d(e), _d(normals), _d(measures), len(e), _d(P), _d(xi_eff), len(P), float(sigma), float(gconst),
-       float(max_angle), int(max_depth), float(eta_min), _d(out.view(np.float64)), _d(resid), _i(clamps))
+    o64 = out.view(np.float64).reshape(len(P), 2)
+    _rows(len(P), lambda i0, i1: fn(_d(e), _d(normals), _d(measures), len(e), _at(P, i0), _at(xi_eff, i0), i1 - i0,
+                                    float(sigma), float(gconst), float(max_angle), int(max_depth), float(eta_min),
+                                    _at(o64, i0), _at(resid, i0), _at(clamps, i0)))
     return out, resid, int(clamps.sum())
 
 

@@ -44,9 +44,13 @@ NO_FMA = {"density.cu"}
 def build(verbose=False, force=False):
     if not force and not needs_build():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
+
     objdir = os.path.join(HERE, "csrc", "_obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    for stale in glob.glob(os.path.join(objdir, "*.o")):
+        os.remove(stale)
+    cmds, objs = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         flags = [f for f in FLAGS if f != "-shared"]
@@ -56,8 +60,12 @@ def build(verbose=False, force=False):
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    # one nvcc per translation unit, concurrently (fft.cu / field.cu dominate)
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as pool:
+        for r in pool.map(lambda c: subprocess.run(c, check=True), cmds):
+            pass
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs], check=True)
     return OUT
 

@@ -39,8 +39,6 @@ SIGNATURES = {
     "gf_cascade_serial": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double,
                                          c_dp, ctypes.c_int, ctypes.c_int64, c_vp, c_vp, c_vp]),
     "gf_measure_fma_peak": (ctypes.c_int, [ctypes.c_int, c_dp]),
-    "gf_set_cascade_variant": (ctypes.c_int, [ctypes.c_int]),
-    "gf_set_cascade_tile": (ctypes.c_int, [ctypes.c_int]),
     "gf_measure_roundtrip": (ctypes.c_int, [ctypes.c_int, c_dp]),
     "gf_measure_launch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_dp, c_dp]),
     "gf_distance_winding": (ctypes.c_int, [ctypes.c_int, c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp]),
@@ -69,13 +67,11 @@ SIGNATURES = {
                                          ctypes.c_int, c_vp, c_vp]),
     "gf_rotate_product_planes": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_dp, c_dp,
                                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
-    "gf_field_zpass": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_int, c_dp, c_dp,
-                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
     "gf_score_field": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_i32p, c_dp, c_dp,
                                       ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
     "gf_set_cascade_debug": (ctypes.c_int, [c_vp]),
     "gf_server_start": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double, c_dp,
-                                       ctypes.c_int, ctypes.c_double, c_u64p]),
+                                       ctypes.c_int, ctypes.c_double, ctypes.c_int, c_u64p]),
     "gf_server_query": (ctypes.c_int, [ctypes.c_uint64, c_dp, c_dp, c_dp]),
     "gf_server_query_fast": (ctypes.c_int, [ctypes.c_uint64, c_vp, c_vp, c_vp]),
     "gf_server_stop": (ctypes.c_int, [ctypes.c_uint64]),
@@ -107,6 +103,9 @@ def _load():
 
 
 LIB = _load()
+
+
+ESTOPPED = -4  # gf status: the haptic server has stopped (idle timeout); fall back to a launch
 
 
 class EngineError(RuntimeError):

@@ -194,9 +194,11 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
             q.R33[...] = R
             q.t3[...] = t_eff
             rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
-            if rc:
+            if rc == 0:
+                return q.res3.copy()
+            if rc != _lib.ESTOPPED:
                 check(rc)
-            return q.res3.copy()
+            srv.retire()  # idle-timed out: this and later calls take the launch path
     arg = q.arg
     if d == 3:
         arg[:9] = R.ravel() if type(R) is np.ndarray else np.asarray(R, dtype=np.float64).ravel()
@@ -210,9 +212,12 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
         arg[15:17] = domega
         arg[14] = arg[17] = 0.0
     srv = _servers.get((W1.handle, W2.handle, bool(wrap), bits)) if _servers else None
+    rc = _lib.ESTOPPED
     if srv is not None and srv.dcell == dcell and arg[12:18].tobytes() == srv.cd_bytes:
         rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
-    else:
+        if rc == _lib.ESTOPPED:
+            srv.retire()
+    if rc == _lib.ESTOPPED:
         rc = LIB.gf_cascade_fast(W1.handle, W2.handle, 1 if wrap else 0, q.pd, float(dcell), q.pR, q.pt, q.pc, bits,
                                  q.pout)
     if rc:
@@ -233,10 +238,15 @@ class HapticServer:
     While it runs, `cascade` calls with the same windows, wrap flag,
     precision and grid constants are answered through its mailbox instead of
     a kernel launch per query.  Use as a context manager (stops on exit); the
-    device side also exits on its own after `idle_timeout_s` without queries.
+    device side also exits on its own after `idle_timeout_s` without queries,
+    after which calls fall back to one launch per query.
+
+    `max_sms` > 0 keeps the resident grid on about that many SMs, leaving the
+    others free for work issued from other threads while the session runs
+    (landscape exports); 0 takes every SM (lowest latency).
     """
 
-    def __init__(self, C1, C2, wrap, domega, dcell, center, precision=None, idle_timeout_s=30.0):
+    def __init__(self, C1, C2, wrap, domega, dcell, center, precision=None, idle_timeout_s=30.0, max_sms=0):
         self.W1, self.W2 = as_device_window(C1), as_device_window(C2)
         d = self.W1.ndim
         self.bits = 64 if (precision or _precision) == "fp64" else 32
@@ -246,7 +256,8 @@ class HapticServer:
         self.center = np.ascontiguousarray(center, dtype=np.float64)[:d].copy()
         sid = ctypes.c_uint64(0)
         check(LIB.gf_server_start(self.W1.handle, self.W2.handle, int(self.wrap), dptr(self.dom), self.dcell,
-                                  dptr(self.center), self.bits, float(idle_timeout_s), ctypes.byref(sid)))
+                                  dptr(self.center), self.bits, float(idle_timeout_s), int(max_sms),
+                                  ctypes.byref(sid)))
         self.id = sid.value
         # one throw-away query: returns once the resident grid is up and its
         # code and windows are warm, so the first real frame pays neither
@@ -275,6 +286,11 @@ class HapticServer:
         if _immutable(center) and _immutable(domega):
             self._c_ref, self._d_ref = center, domega
         return True
+
+    def retire(self):
+        """The device side has exited (idle timeout): stop routing calls here."""
+        if _servers.get(self.key) is self:
+            del _servers[self.key]
 
     def stop(self):
         if self.id:

@@ -13,7 +13,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -47,6 +49,54 @@ static void server_stopped() {
     for (void* p : g_deferred) cudaFree(p);
     g_deferred.clear();
   }
+}
+
+// ---------------------------------------------------------------------------
+// per-device launch caches (common.cuh)
+
+static std::mutex g_attr_mu;
+static std::map<std::pair<const void*, int>, size_t> g_smem_set;
+static std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+static std::map<int, int> g_sms;
+
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+cudaError_t ensure_smem(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  size_t& have = g_smem_set[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+int sm_count() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_sms.find(dev);
+  if (it != g_sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 1;
+  g_sms[dev] = n;
+  return n;
+}
+
+int resident_ctas(const void* func, int threads, size_t smem) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto key = std::make_tuple(func, dev, threads, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, func, threads, smem) != cudaSuccess || n < 1) n = 1;
+  g_occ[key] = n;
+  return n;
 }
 
 // ---------------------------------------------------------------------------
@@ -98,22 +148,35 @@ struct Context {
   int64_t partials_cap = 0, counters_cap = 0;
 };
 static thread_local Context tl_ctx;
-static int g_run_length = 0;
-static int g_variant = 1;
-static int g_tile = 0;
-static unsigned long long* g_debug = nullptr;
+static std::atomic<int> g_run_length{0};
+static std::atomic<unsigned long long*> g_debug{nullptr};
 
 static int ensure_context() {
   int dev = 0;
   GF_CUDA(cudaGetDevice(&dev));
   Context& c = tl_ctx;
   if (c.device == dev && c.stream) return 0;
+  // first use on this thread, or the thread moved to another device: the
+  // stream, mapped slots, scratch and cached launch all belong to the old one
+  // (the old device's allocations are left to the process; switching devices
+  // per thread is rare)
+  c.cached = false;
+  c.partials = nullptr;
+  c.counters = nullptr;
+  c.partials_cap = c.counters_cap = 0;
+  c.seq = 0;
   int lo = 0, hi = 0;
   GF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   GF_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi));
   GF_CUDA(cudaHostAlloc((void**)&c.host_out, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
   std::memset(c.host_out, 0, 64 * sizeof(unsigned long long));
   GF_CUDA(cudaHostGetDevicePointer((void**)&c.dev_out_alias, c.host_out, 0));
+  // stream-ordered scratch (scratch_acquire) stays in the device pool between calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long keep = 64ull << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   c.device = dev;
   return 0;
 }
@@ -134,6 +197,29 @@ static int ensure_scratch(Context& c, int64_t n_partials, int64_t n_counters, cu
     c.counters_cap = n_counters;
   }
   return 0;
+}
+
+// Scratch of the entry points that run on the CALLER's stream (batched
+// sweep, serial loop): allocated, zeroed and released in that stream's order,
+// so concurrent calls on other streams -- or a single query on the thread's
+// own stream -- never share a ticket counter or partials.
+struct StreamScratch {
+  double* partials = nullptr;
+  unsigned* counters = nullptr;
+};
+
+static int scratch_acquire(int64_t n_partials, int64_t n_counters, cudaStream_t st, StreamScratch& s) {
+  GF_CUDA(cudaMallocAsync((void**)&s.partials, (size_t)n_partials * sizeof(double), st));
+  GF_CUDA(cudaMallocAsync((void**)&s.counters, (size_t)n_counters * sizeof(unsigned), st));
+  GF_CUDA(cudaMemsetAsync(s.counters, 0, (size_t)n_counters * sizeof(unsigned), st));
+  return 0;
+}
+
+static void scratch_release(StreamScratch& s, cudaStream_t st) {
+  if (s.partials) cudaFreeAsync(s.partials, st);
+  if (s.counters) cudaFreeAsync(s.counters, st);
+  s.partials = nullptr;
+  s.counters = nullptr;
 }
 
 // raw (complex<T>) and packed moving-operand layouts, built lazily once
@@ -195,8 +281,7 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
   std::memset(&a, 0, sizeof a);
   int rc = window_raw(w1, precision, st, &a.C1);
   if (rc) return rc;
-  if (g_variant == 0) rc = window_raw(w2, precision, st, &a.C2p);
-  else rc = window_packed(w2, precision, wrap, st, &a.C2p);
+  rc = window_packed(w2, precision, wrap, st, &a.C2p);
   if (rc) return rc;
   for (int ax = 0; ax < 3; ++ax) a.w[ax] = w1->w[ax];
   a.dim = w1->d;
@@ -210,10 +295,8 @@ static int fill_args(CascadeArgs& a, Window* w1, Window* w2, int wrap, const dou
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) a.rdom[i][j] = a.dom[i] / a.dom[j];
   a.dcell = dcell;
-  a.seg_len = g_run_length;
-  a.variant = g_variant;
-  a.tile_force = g_tile;
-  a.debug = g_debug;
+  a.seg_len = g_run_length.load();
+  a.debug = g_debug.load();
   return 0;
 }
 
@@ -336,28 +419,16 @@ int gf_window_device_ptr(uint64_t handle, const void** dev_c128) {
   return 0;
 }
 
-int gf_set_cascade_variant(int v) {
-  GF_CHECK(v == 0 || v == 1, GF_EINVAL, "variant must be 0 (tiled) or 1 (direct)");
-  g_variant = v;
-  return 0;
-}
-
 // Debug: per-block phase timestamps of the single-query kernel (device
 // buffer of >= 8 * blocks uint64, or null to disable).
 int gf_set_cascade_debug(void* dev_buf) {
-  g_debug = (unsigned long long*)dev_buf;
-  return 0;
-}
-
-int gf_set_cascade_tile(int ts) {
-  GF_CHECK(ts == 0 || ts == 8 || ts == 16, GF_EINVAL, "tile must be 0 (auto), 8 or 16");
-  g_tile = ts;
+  g_debug.store((unsigned long long*)dev_buf);
   return 0;
 }
 
 int gf_set_cascade_run_length(int L) {
   GF_CHECK(L >= 0 && L <= 1024, GF_EINVAL, "run length out of range");
-  g_run_length = L;
+  g_run_length.store(L);
   return 0;
 }
 
@@ -375,13 +446,13 @@ int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double 
   // frame: reuse the planned launch, only the pose changes
   const bool hit = c.cached && c.ch1 == h1 && c.ch2 == h2 && c.cwrap == (wrap ? 1 : 0) && c.cprec == precision &&
                    c.cdcell == dcell && std::memcmp(c.cdom, domega, d * sizeof(double)) == 0 &&
-                   std::memcmp(c.ccen, center, d * sizeof(double)) == 0 && g_debug == c.cargs.debug;
+                   std::memcmp(c.ccen, center, d * sizeof(double)) == 0 && g_debug.load() == c.cargs.debug;
   if (!hit) {
     CascadeArgs a;
     rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, c.stream);
     if (rc) return rc;
     a.poses = nullptr;
-    plan_cascade(a, 1, 2 * 148);
+    plan_cascade(a, 1, 2 * sm_count());
     rc = ensure_scratch(c, (int64_t)a.blocks_per_pose * kNumMoments, 1, c.stream);
     if (rc) return rc;
     a.partials = c.partials;
@@ -447,15 +518,18 @@ int gf_cascade_batch(uint64_t h1, uint64_t h2, int wrap, const double* domega, d
   rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, st);
   if (rc) return rc;
   a.poses = poses_dev;
-  plan_cascade(a, n, 4 * 148);
+  plan_cascade(a, n, 4 * sm_count());
+  StreamScratch sc;
   if (a.blocks_per_pose > 1) {
-    rc = ensure_scratch(tl_ctx, n * a.blocks_per_pose * kNumMoments, n, st);
+    rc = scratch_acquire(n * a.blocks_per_pose * kNumMoments, n, st, sc);
     if (rc) return rc;
-    a.partials = tl_ctx.partials;
-    a.counters = tl_ctx.counters;
+    a.partials = sc.partials;
+    a.counters = sc.counters;
   }
   a.out = out_dev;
-  GF_CUDA(launch_cascade(a, n, st));
+  cudaError_t le = launch_cascade(a, n, st);
+  scratch_release(sc, st);
+  GF_CUDA(le);
   return 0;
 }
 
@@ -472,17 +546,21 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   CascadeArgs a;
   rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, st);
   if (rc) return rc;
-  plan_cascade(a, 1, 2 * 148);
-  rc = ensure_scratch(tl_ctx, (int64_t)a.blocks_per_pose * kNumMoments, 1, st);
+  plan_cascade(a, 1, 2 * sm_count());
+  StreamScratch sc;
+  rc = scratch_acquire((int64_t)a.blocks_per_pose * kNumMoments, 1, st, sc);
   if (rc) return rc;
-  a.partials = tl_ctx.partials;
-  a.counters = tl_ctx.counters;
+  a.partials = sc.partials;
+  a.counters = sc.counters;
   // one single-query launch per pose, stream-ordered (the haptic loop shape)
-  for (int64_t i = 0; i < n; ++i) {
+  cudaError_t le = cudaSuccess;
+  for (int64_t i = 0; i < n && le == cudaSuccess; ++i) {
     a.poses = poses_dev + 12 * i;
     a.out = out_dev + 14 * i;
-    GF_CUDA(launch_cascade(a, 1, st));
+    le = launch_cascade(a, 1, st);
   }
+  scratch_release(sc, st);
+  GF_CUDA(le);
   return 0;
 }
 
@@ -541,7 +619,7 @@ int stop_server(Server* s) {
 }  // namespace
 
 int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, double dcell, const double* center,
-                    int precision, double idle_timeout_s, uint64_t* server_id) {
+                    int precision, double idle_timeout_s, int max_sms, uint64_t* server_id) {
   GF_CHECK(domega && center && server_id, GF_EINVAL, "null argument");
   int rc = ensure_context();
   if (rc) return rc;
@@ -556,8 +634,8 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, do
   CascadeArgs a;
   rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, s->stream);
   if (rc) return rc;
-  GF_CHECK(a.variant == 1, GF_EINVAL, "the haptic server needs the default (direct) cascade variant");
-  plan_cascade(a, 1, 2 * 148);
+  GF_CHECK(max_sms >= 0, GF_EINVAL, "max_sms must be >= 0 (0: every SM)");
+  plan_cascade(a, 1, 2 * sm_count());
   GF_CHECK(a.single == 1, GF_EINTERNAL, "single-pose plan expected");
   GF_CUDA(cudaHostAlloc((void**)&s->mb, sizeof(Mailbox), cudaHostAllocMapped));
   std::memset((void*)s->mb, 0, sizeof(Mailbox));
@@ -565,26 +643,24 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, do
   GF_CUDA(cudaMalloc(&s->dev_words, 32 * sizeof(unsigned long long)));
   GF_CUDA(cudaMemsetAsync(s->dev_words, 0, 32 * sizeof(unsigned long long), s->stream));
   GF_CUDA(cudaMalloc((void**)&s->partials, (size_t)a.blocks_per_pose * kNumMoments * sizeof(double)));
-  GF_CUDA(cudaMalloc((void**)&s->counters, sizeof(unsigned)));
-  GF_CUDA(cudaMemsetAsync(s->counters, 0, sizeof(unsigned), s->stream));
+  GF_CUDA(cudaMalloc((void**)&s->counters, 4 * sizeof(unsigned)));  // [0] ticket, [2..3] enlist
+  GF_CUDA(cudaMemsetAsync(s->counters, 0, 4 * sizeof(unsigned), s->stream));
   a.partials = s->partials;
   a.counters = s->counters;
   a.out = nullptr;
   a.ll_out = const_cast<unsigned long long*>(s->mb_dev->out);
-  a.debug = g_debug;  // null unless gf_set_cascade_debug armed it
+  a.debug = g_debug.load();  // null unless gf_set_cascade_debug armed it
   ServerCtl ctl;
   ctl.host_req = s->mb_dev->req;
   ctl.dev_req = (volatile unsigned long long*)s->dev_words;
   ctl.start_seq = 0;
   ctl.idle_timeout_ns = (unsigned long long)((idle_timeout_s > 0 ? idle_timeout_s : 30.0) * 1e9);
-  auto tl0 = std::chrono::steady_clock::now();
+  ctl.sm_limit = max_sms > 0 ? max_sms : 1 << 30;
+  ctl.enlist = s->counters + 2;
   server_started();
   cudaError_t le = launch_cascade_server(a, ctl, s->stream);
   if (le != cudaSuccess) server_stopped();
   GF_CUDA(le);
-  if (getenv("GF_DEBUG_SERVER"))
-    fprintf(stderr, "[gf] server launch took %.3f ms\n",
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count());
   s->d = w1->d;
   s->running = true;
   std::lock_guard<std::mutex> lk(g_srv_mu);
@@ -596,7 +672,7 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, do
 int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, double* out) {
   Server* s = find_server(server_id);
   GF_CHECK(s && R && t_eff && out, GF_EINVAL, "unknown server or null argument");
-  GF_CHECK(s->running, GF_EINVAL, "server is not running (stopped or idle-timed out)");
+  GF_CHECK(s->running, GF_ESTOPPED, "server is not running (stopped or idle-timed out)");
   double pose[12];
   embed_pose(s->d, R, t_eff, pose);
   post_request(s, pose, 0u);
@@ -609,7 +685,7 @@ int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, do
       s->running = false;
       server_stopped();
       if (e != cudaSuccess) GF_CUDA(e);
-      GF_CHECK(false, GF_EINVAL, "server exited (idle timeout); start a new one");
+      GF_CHECK(false, GF_ESTOPPED, "server exited (idle timeout); start a new one");
     }
     GF_CHECK(std::chrono::steady_clock::now() - t0 < std::chrono::seconds(5), GF_EINTERNAL,
              "haptic server did not answer within 5 s");

@@ -441,7 +441,7 @@ cudaError_t launch_pack_window(int precision, const void* raw, void* packed, con
                                cudaStream_t st) {
   int64_t n = packed_window_elems(w);
   int grid = (int)ceil_div(n, 256);
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > sm_count() * 16) grid = sm_count() * 16;
   if (precision == 32)
     pack_window_kernel<float><<<grid, 256, 0, st>>>((const cx<float>*)raw, (float4*)packed, w[0], w[1], w[2], wrap);
   else
@@ -451,7 +451,7 @@ cudaError_t launch_pack_window(int precision, const void* raw, void* packed, con
 
 cudaError_t launch_narrow(const void* src, void* dst, int64_t n, cudaStream_t st) {
   int grid = (int)ceil_div(n, 256);
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > sm_count() * 16) grid = sm_count() * 16;
   narrow_kernel<float><<<grid, 256, 0, st>>>((const cx<double>*)src, (cx<float>*)dst, n);
   return cudaGetLastError();
 }
@@ -469,22 +469,9 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
   double floor_eps = (a.precision == 32) ? 1e-4 : 1e-9;
   a.tie_eps = eps > floor_eps ? eps : floor_eps;
 
-  if (a.variant == 0) {
-    // u-space tiles: small tiles for a lone query (latency), large for sweeps
-    a.tile = (a.precision == 32 && n_poses >= target_blocks / 2) ? 16 : 8;
-    if (a.tile_force && (a.precision == 32 || a.tile_force == 8)) a.tile = a.tile_force;
-    int tiles = tiled_tile_count(a, a.tile);
-    int64_t bpp = 1;
-    if (n_poses < target_blocks) bpp = ceil_div(target_blocks, n_poses);
-    if (bpp > tiles) bpp = tiles;
-    a.blocks_per_pose = (int)bpp;
-    a.smem_bytes = (int)tiled_smem_bytes(a.precision, a.tile, a.w);
-    return;
-  }
-  if (n_poses == 1 && a.variant == 1) {
+  if (n_poses == 1) {
     a.single = 1;
     a.blocks_per_pose = single_blocks(a, target_blocks / 2);
-    a.tile = 0;  // single kernel: contiguous unit ranges per CTA (segment loop)
     return;
   }
   a.single = 0;
@@ -517,7 +504,6 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
 }
 
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st) {
-  if (a.variant == 0) return launch_cascade_tiled(a, n_poses, st);
   if (a.single && n_poses == 1) return launch_cascade_single(a, st);
   // grid.x = poses x blocks_per_pose, issued in chunks that fit gridDim.x
   const int64_t max_blocks = (int64_t)1 << 30;

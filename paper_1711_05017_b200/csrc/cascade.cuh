@@ -30,10 +30,6 @@ struct CascadeArgs {
   int blocks_per_pose;
   int64_t segs_per_block;
   double tie_eps;
-  int variant;           // 0 = u-space tiled (default), 1 = direct gather
-  int tile;              // tiled variant: cells per tile side (8 or 16)
-  int tile_force;        // 0 = auto
-  int smem_bytes;        // tiled variant: dynamic shared memory per CTA
   int single;            // 1: one pose through the latency kernel (cascade_single.cu)
   // cross-block scratch and output
   double* partials;      // n_poses * blocks_per_pose * kNumMoments (if bpp > 1)
@@ -82,14 +78,13 @@ struct ServerCtl {
   volatile unsigned long long* dev_req;         // device copy forwarded by CTA 0
   unsigned long long start_seq;
   unsigned long long idle_timeout_ns;
+  int sm_limit;         // clusters whose rank 0 runs on an SM id >= sm_limit leave at start
+  unsigned* enlist;     // 2 zeroed device counters: clusters decided, clusters serving
 };
 cudaError_t launch_cascade_server(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st);
 
-int tiled_tile_count(const CascadeArgs& a, int ts);
-size_t tiled_smem_bytes(int precision, int ts, const int w[3]);
 int single_blocks(const CascadeArgs& a, int sms);
 cudaError_t launch_cascade_single(const CascadeArgs& a, cudaStream_t st);
-cudaError_t launch_cascade_tiled(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);
 void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks);
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);
 int64_t packed_window_elems(const int w[3]);

@@ -28,7 +28,6 @@
 #include <cuda/atomic>
 
 #include <math.h>
-#include <stdlib.h>
 
 namespace gf {
 namespace {
@@ -38,7 +37,7 @@ constexpr int kThreads = 256;
 // at c * kTrLd + s + 8 i -- hit 32 distinct banks (fp32) / distinct 8-byte
 // slots per half-warp (fp64)
 constexpr int kTrLd = kThreads + 8;
-int g_cluster = 4;  // CTAs per cluster (DSMEM reduction stage); 1 disables
+constexpr int kCluster = 4;  // CTAs per cluster (DSMEM reduction stage; measured best, profiles/r01_summary.md)
 
 struct SinglePose {
   double mu[3][3];
@@ -58,6 +57,7 @@ struct SinglePose {
 // and arrive on `bar` (release.cluster); rank 0 waits on it (acquire) -- a
 // one-way hand-off, no cluster-wide barrier on the query path.
 constexpr int kMaxCluster = 8;
+static_assert(kCluster <= kMaxCluster, "cluster stage sized for kMaxCluster ranks");
 // resident CTAs per SM the register budget is sized for: the server grid is
 // 2 x 148 CTAs (up to 128 registers); the one-shot kernel keeps room for a
 // third so the next launch's CTAs can start beside the previous tail
@@ -161,7 +161,7 @@ __device__ __forceinline__ void emit_output(const CascadeArgs& a, int i, double 
 template <typename T, bool WRAP>
 __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const double* src, SinglePose& sp, double* red,
                                                  unsigned& ticket, ClusterRed& cr, unsigned char* smem_raw,
-                                                 unsigned long long done_seq) {
+                                                 unsigned long long done_seq, int vb, int vg) {
   using P4 = typename pair4<T>::type;
   // dynamic: transpose buffer tr[26][257] (reduction) | px | py | pz
   T(*tr)[kTrLd] = reinterpret_cast<T(*)[kTrLd]>(smem_raw);
@@ -176,7 +176,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   cx<T>* ttab = ptab + (a.w[0] + a.w[1] + a.w[2]);
 
   const int tid = threadIdx.x;
-  unsigned long long* dbg = a.debug ? a.debug + (int64_t)blockIdx.x * 8 : nullptr;
+  unsigned long long* dbg = a.debug ? a.debug + (int64_t)vb * 8 : nullptr;
 #define GF_STAMP(k)                                                                 \
   if (dbg && tid == 0) {                                                           \
     unsigned long long t_;                                                         \
@@ -290,8 +290,8 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   // exact integer add per axis, C1 by one stride, and the seven per-mode
   // products go into 8 run sums (sum Y, sum j Y) folded into the 26 moments
   // once per segment -- the batched sweep's loop shape (cascade.cu).
-  const int upb = (units + gridDim.x - 1) / gridDim.x;
-  const int u_begin = blockIdx.x * upb;
+  const int upb = (units + vg - 1) / vg;
+  const int u_begin = vb * upb;
   const int u_end = min(units, u_begin + upb);
   const cx<T>* pt_p = ptab + (p == 0 ? 0 : (p == 1 ? w0 : w0 + w1));
   const cx<T>* pt_q = ptab + (q == 0 ? 0 : (q == 1 ? w0 : w0 + w1));
@@ -485,7 +485,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   if (c < kNumMoments && s == 0) red[c] = part;
   __syncthreads();
 
-  const int bpp = gridDim.x;
+  const int bpp = vg;
   if (bpp == 1) {
     if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
     return;
@@ -496,7 +496,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   unsigned crank, csize;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
-  const int cid = blockIdx.x / (int)csize, nclusters = gridDim.x / (int)csize;
+  const int cid = vb / (int)csize, nclusters = vg / (int)csize;
   if (csize > 1) {
     if (cr.armed) {  // rank 0's barrier init is visible once the start barrier completes
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
@@ -576,16 +576,60 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? kMinBlocksLaunch : 
   if (threadIdx.x < 12)
     pose_s[threadIdx.x] = a.poses ? a.poses[a.pose_offset * 12 + threadIdx.x] : a.pose_inline[threadIdx.x];
   cluster_red_init(cr);  // ends with __syncthreads
-  single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, a.done_seq);
+  single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, a.done_seq, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
 // Persistent haptic server: the grid stays resident (cooperative launch) and
-// serves one query per mailbox sequence number.  Block 0 polls the host-
-// mapped mailbox and forwards the pose to device memory; the other blocks
-// poll a device word.  No kernel launch per query.
+// serves one query per mailbox sequence number.  The lead CTA polls the host-
+// mapped mailbox and forwards the pose to device memory; the other CTAs poll
+// that device copy.  No kernel launch per query.
+//
+// SM budget (landscape exports run while a session serves
+// frames): the grid is launched on every SM, then each cluster whose rank-0
+// CTA sits on an SM id >= ctl.sm_limit exits at once, so those SMs stay free
+// for other kernels for the whole session.  Survivors take dense virtual
+// cluster ids from a device counter and split the modes among themselves.
 constexpr unsigned long long kServerStop = ~0ull;
-constexpr int kPollWarps = 2;  // CTA 0 warps polling the host mailbox
+constexpr int kPollWarps = 2;  // lead-CTA warps polling the host mailbox
+
+// one-time start-up: decide survival per cluster and hand out virtual ids.
+// Returns false when this CTA's cluster leaves the server.
+__device__ __forceinline__ bool server_enlist(const ServerCtl& ctl, int& vb, int& vg) {
+  __shared__ int s_vcid, s_nsurv;
+  unsigned crank, csize, smid;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const unsigned nclusters = gridDim.x / csize;
+  if (threadIdx.x == 0) s_vcid = -1;
+  __syncthreads();
+  if (crank == 0 && threadIdx.x == 0) {
+    // cluster 0 always serves, so at least one cluster survives any budget
+    const bool keep = (blockIdx.x == 0) || smid < (unsigned)ctl.sm_limit;
+    if (keep) s_vcid = (int)atomicAdd(ctl.enlist + 1, 1u);
+    __threadfence();
+    atomicAdd(ctl.enlist, 1u);
+    // every cluster has decided once the first counter reaches the launch count
+    while (*(volatile unsigned*)ctl.enlist < nclusters) __nanosleep(100);
+    __threadfence();
+    s_nsurv = (int)*(volatile unsigned*)(ctl.enlist + 1);
+  }
+  // rank 0's decision to the other ranks of the cluster (DSMEM read)
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  int vcid, nsurv;
+  {
+    unsigned a0 = map_rank0(smem_addr(&s_vcid)), a1 = map_rank0(smem_addr(&s_nsurv));
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(vcid) : "r"(a0) : "memory");
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(nsurv) : "r"(a1) : "memory");
+  }
+  // rank 0 must not exit while peers still read its shared memory
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (vcid < 0) return false;
+  vb = vcid * (int)csize + (int)crank;
+  vg = nsurv * (int)csize;
+  return true;
+}
 
 template <typename T, bool WRAP>
 __global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_kernel(CascadeArgs a,
@@ -597,61 +641,63 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_k
   __shared__ unsigned long long cur;
   __shared__ double pose_s[12];
   __shared__ ClusterRed cr;
+  int vb = 0, vg = 1;
+  if (!server_enlist(ctl, vb, vg)) return;  // this SM stays free for other work
   cluster_red_init(cr);
   unsigned long long last = ctl.start_seq;
   const int tid = threadIdx.x;
-  __shared__ int found;  // CTA 0: a polling warp has the request
+  const bool lead = vb == 0;
+  __shared__ int found;  // lead CTA: which warp owns this request (0 = none yet)
   while (true) {
     const unsigned expect = (unsigned)(last + 1);
     if (tid == 0) found = 0;
     __syncthreads();
-    // CTA 0 polls the host mailbox with kPollWarps warps whose polls are
-    // staggered in time: a PCIe read takes ~1 us, so several reads in flight
-    // cut the wait between the host's write and its detection
-    const int pollers = blockIdx.x == 0 ? kPollWarps : 1;
+    // the lead CTA polls the host mailbox with kPollWarps warps whose polls
+    // are staggered in time: a PCIe read takes ~1 us, so several reads in
+    // flight cut the wait between the host's write and its detection.  The
+    // first warp to see a complete request (or, warp 0 only, the idle
+    // deadline) claims it with a CAS on `found`; only the owner forwards it.
+    const int pollers = lead ? kPollWarps : 1;
     if (tid < 32 * pollers) {
-      // warp 0: lanes 0..24 read the 25 request slots in one instruction and
-      // the warp votes; CTA 0 polls the host mailbox (one PCIe round trip per
-      // poll, the pose arrives with the tags) and forwards the slots to device
-      // memory, the other CTAs poll that copy in L2
       const int lane = tid & 31;
       unsigned long long v = 0;
-      bool ok;
-      bool publish = true;
-      if (blockIdx.x == 0) {
+      bool mine = true;
+      if (lead) {
         const int pw = tid >> 5;
         unsigned long long t0, t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         do {  // stagger the start of warp pw by pw / kPollWarps of a PCIe round trip
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         } while (t1 - t0 < (unsigned long long)(pw * 1000 / kPollWarps));
-        bool mine = false;
+        mine = false;
         while (true) {
           if (lane < kReqSlots) v = ctl.host_req[lane];
-          ok = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
-          if (ok) {
-            mine = true;
+          bool got = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
+          bool stop_now = false;
+          if (!got && pw == 0) {  // only warp 0 may give up on idleness
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            stop_now = t1 - t0 > ctl.idle_timeout_ns;
+          }
+          if (got || stop_now) {
+            int won = 0;
+            if (lane == 0) won = atomicCAS(&found, 0, pw + 1) == 0;
+            won = __shfl_sync(0xffffffffu, won, 0);
+            if (won) {
+              mine = true;
+              if (!got)  // idle: forward a stop request under this sequence number
+                v = lane == kReqSlots - 1 ? (((unsigned long long)expect << 32) | 1ull)
+                                          : ((unsigned long long)expect << 32);
+            }
             break;
           }
           const int other = __shfl_sync(0xffffffffu, lane == 0 ? *(volatile int*)&found : 0, 0);
-          if (other) break;  // another warp got it (warp-uniform)
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-          if (t1 - t0 > ctl.idle_timeout_ns) {  // idle: forward a stop request
-            v = lane == kReqSlots - 1 ? (((unsigned long long)expect << 32) | 1ull)
-                                      : ((unsigned long long)expect << 32);
-            mine = true;
-            break;
-          }
+          if (other) break;  // another warp owns the request (warp-uniform)
         }
-        publish = mine;  // only a detecting warp forwards and assembles
-        if (mine) {
-          if (lane < kReqSlots) ctl.dev_req[lane] = v;
-          if (lane == 0) *(volatile int*)&found = 1;
-        }
+        if (mine && lane < kReqSlots) ctl.dev_req[lane] = v;
       } else {
         while (true) {
           if (lane < kReqSlots) v = ctl.dev_req[lane];
-          ok = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
+          const bool ok = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
           if (ok) break;
           __nanosleep(20);
         }
@@ -660,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_k
       const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, (2 * lane) & 31);
       const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)v, (2 * lane + 1) & 31);
       const unsigned stopw = __shfl_sync(0xffffffffu, (unsigned)v, kReqSlots - 1);
-      if (publish) {  // duplicate detections in CTA 0 write identical values
+      if (mine) {
         if (lane < 12) pose_s[lane] = __hiloint2double((int)hi, (int)lo);
         if (lane == 0) cur = stopw ? kServerStop : last + 1;
       }
@@ -671,24 +717,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_k
     if (a.debug && tid == 0) {  // when this CTA saw the query
       unsigned long long t_;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      a.debug[(int64_t)blockIdx.x * 8 + 7] = t_;
+      a.debug[(int64_t)vb * 8 + 7] = t_;
     }
-    single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, sq);
+    single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, sq, vb, vg);
     last = sq;
     __syncthreads();
   }
+  // a cluster's CTAs must not exit while a peer may still push into rank 0
+  // (complete the start-up phase first if no query ever waited on it)
+  if (cr.armed) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 template <typename T, bool WRAP>
 cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
   size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + 2 * sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
-  static size_t configured = 0;
-  if (smem > configured && smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(cascade3d_single_kernel<T, WRAP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = ensure_smem((const void*)cascade3d_single_kernel<T, WRAP>, smem);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)a.blocks_per_pose);
   cfg.blockDim = dim3(kThreads);
@@ -696,7 +741,7 @@ cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = g_cluster;
+  attr[0].val.clusterDim.x = kCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -714,34 +759,23 @@ int single_blocks(const CascadeArgs& a, int sms) {
     int64_t u = ceil_div(a.w[o1], 16) * ceil_div(a.w[o2], 16) * a.w[r];
     if (best == 0 || u < best) best = u;
   }
-  int64_t target = (int64_t)sms * 2;  // 2 CTAs per SM: one resident wave, measured best (profiles/r01_cascade_notes.md)
-  if (const char* env = getenv("GF_SINGLE_BLOCKS")) target = atoi(env);  // experiments only
+  const int64_t target = (int64_t)sms * 2;  // 2 CTAs per SM: one resident wave, measured best (profiles/r01_cascade_notes.md)
   // equal work per CTA: the largest count <= target that gives every CTA the
   // same number of units (no straggler CTA with one extra unit)
   int64_t b = best < target ? best : target;
   if (best > target) b = best / ceil_div(best, target);
-  if (const char* env = getenv("GF_SINGLE_CLUSTER")) g_cluster = atoi(env);  // experiments only
-  if (g_cluster < 1) g_cluster = 1;
-  if (g_cluster > kMaxCluster) g_cluster = kMaxCluster;
-  b = (b / g_cluster) * g_cluster;  // whole clusters
-  return (int)(b < g_cluster ? g_cluster : b);
+  b = (b / kCluster) * kCluster;  // whole clusters
+  return (int)(b < kCluster ? kCluster : b);
 }
 
 template <typename T, bool WRAP>
 cudaError_t launch_server_t(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st) {
   size_t smem = sizeof(T) * kNumMoments * kTrLd + 16 + 2 * sizeof(cx<T>) * (a.w[0] + a.w[1] + a.w[2]);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(cascade3d_server_kernel<T, WRAP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cascade3d_server_kernel<T, WRAP>, kThreads,
-                                                                smem);
+  const void* fn = (const void*)cascade3d_server_kernel<T, WRAP>;
+  cudaError_t e = ensure_smem(fn, smem);
   if (e != cudaSuccess) return e;
-  if ((int64_t)per_sm * sms < a.blocks_per_pose) return cudaErrorCooperativeLaunchTooLarge;
+  const int per_sm = resident_ctas(fn, kThreads, smem);
+  if ((int64_t)per_sm * sm_count() < a.blocks_per_pose) return cudaErrorCooperativeLaunchTooLarge;
   // co-residency guaranteed (cooperative) and the same CTA clusters as the
   // one-shot kernel (DSMEM hand-off stage)
   cudaLaunchConfig_t cfg = {};
@@ -753,19 +787,18 @@ cudaError_t launch_server_t(const CascadeArgs& a, const ServerCtl& ctl, cudaStre
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = g_cluster;
+  attr[1].val.clusterDim.x = kCluster;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   e = cudaLaunchKernelEx(&cfg, cascade3d_server_kernel<T, WRAP>, a, ctl);
   if (e == cudaSuccess) return e;
-  (void)cudaGetLastError();  // clusters + cooperative refused: plain cooperative launch
-  CascadeArgs aa = a;
-  ServerCtl cc = ctl;
-  void* args[] = {&aa, &cc};
-  return cudaLaunchCooperativeKernel((const void*)cascade3d_server_kernel<T, WRAP>, dim3(a.blocks_per_pose),
-                                     dim3(kThreads), args, smem, st);
+  // clusters + cooperative refused (large fp64 windows): one-CTA clusters,
+  // i.e. a plain cooperative launch -- the same body with csize = 1
+  (void)cudaGetLastError();
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cascade3d_server_kernel<T, WRAP>, a, ctl);
 }
 
 cudaError_t launch_cascade_server(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st) {

@@ -17,6 +17,7 @@ enum GfStatus : int {
   GF_EINVAL = -1,   // bad argument (shape, handle, dtype)
   GF_ENOMEM = -2,   // host allocation failure
   GF_EINTERNAL = -3,
+  GF_ESTOPPED = -4, // haptic server no longer running (stopped / idle timeout)
 };
 
 void set_error(const std::string& msg);
@@ -26,6 +27,17 @@ const char* last_error();
 // grid is resident that would wait for its idle timeout.  All engine frees go
 // through device_free, which defers them until no server is running.
 void device_free(void* p);
+
+// Per-device launch plumbing (capi.cu), thread-safe: the attribute and
+// occupancy caches are keyed by (kernel, device), so a second device in the
+// same process gets its own cudaFuncSetAttribute and SM count.
+//   ensure_smem   raise `func`'s dynamic shared-memory limit to >= bytes
+//                 (no-op below the 48 KB default) on the current device;
+//   sm_count      multiprocessor count of the current device;
+//   resident_ctas CTAs of `func` resident per SM at (threads, smem), >= 1.
+cudaError_t ensure_smem(const void* func, size_t bytes);
+int sm_count();
+int resident_ctas(const void* func, int threads, size_t smem);
 
 #define GF_CUDA(expr)                                                            \
   do {                                                                           \

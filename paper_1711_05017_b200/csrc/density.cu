@@ -672,7 +672,7 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
   if (family != 0) {
     // xi_eff = max(xi, eta_min) (descriptor.py:338)
     GF_CUDA(dxe.alloc(sizeof(double) * m));
-    clamp_min_kernel<<<148 * 8, 256, 0, st>>>((const double*)dxi.p, (double*)dxe.p, m, eta_min);
+    clamp_min_kernel<<<sm_count() * 8, 256, 0, st>>>((const double*)dxi.p, (double*)dxe.p, m, eta_min);
     GF_CUDA(cudaGetLastError());
     SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
     if (d == 3)
@@ -686,11 +686,11 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     GF_CUDA(cudaGetLastError());
   }
   GF_CUDA(cudaEventRecord(ev[2], st));
-  combine_kernel<<<148 * 8, 256, 0, st>>>(m, (const double*)dxi.p, (const double*)dwind.p, (const double*)dip.p,
+  combine_kernel<<<sm_count() * 8, 256, 0, st>>>(m, (const double*)dxi.p, (const double*)dwind.p, (const double*)dip.p,
                                           (const double*)dres.p, family, lam_in, lam_out, eta_min, max_angle,
                                           (double*)dval.p, out_flags);
   GF_CUDA(cudaGetLastError());
-  neighbor_fill_kernel<<<148 * 8, 256, 0, st>>>(d, src.dims[0], src.dims[1], d == 3 ? src.dims[2] : 1,
+  neighbor_fill_kernel<<<sm_count() * 8, 256, 0, st>>>(d, src.dims[0], src.dims[1], d == 3 ? src.dims[2] : 1,
                                                 (const double*)dval.p, out_flags, (double*)out_vals);
   GF_CUDA(cudaGetLastError());
   if (halos) {
@@ -701,7 +701,7 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
   DevBuf dst;
   GF_CUDA(dst.alloc(2 * sizeof(unsigned long long)));
   GF_CUDA(cudaMemsetAsync(dst.p, 0, 2 * sizeof(unsigned long long), st));
-  stats_kernel<<<148 * 4, 256, 0, st>>>((const double*)dres.p + off, (const int64_t*)dcl.p + off, own,
+  stats_kernel<<<sm_count() * 4, 256, 0, st>>>((const double*)dres.p + off, (const int64_t*)dcl.p + off, own,
                                         (unsigned long long*)dst.p);
   GF_CUDA(cudaGetLastError());
   unsigned long long hs[2];

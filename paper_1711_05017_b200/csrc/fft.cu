@@ -616,14 +616,9 @@ cudaError_t launch_scatter_n(const FftArgs& a, const ScatterOut& so, cudaStream_
   constexpr int B0 = 128 / sizeof(cx<T>);
   constexpr int B = B0 * TPL > 1024 ? 1024 / TPL : B0;
   constexpr size_t smem = sizeof(cx<T>) * B * LineLD<T, N>::value;
-  if (smem > 48 * 1024) {
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(fft_scatter_kernel<T, N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+  {
+    cudaError_t e = ensure_smem((const void*)fft_scatter_kernel<T, N, B>, smem);
+    if (e != cudaSuccess) return e;
   }
   const int64_t blocks = (int64_t)a.shape_in[0] * ceil_div(a.shape_in[2], B);
   fft_scatter_kernel<T, N, B><<<(unsigned)blocks, B * TPL, smem, st>>>(a, so);
@@ -688,21 +683,12 @@ cudaError_t launch_nb(const FftArgs& a, cudaStream_t st) {
     blocks = (int64_t)so * ceil_div(a.shape_in[2], B);
   }
   constexpr size_t smem = sizeof(cx<T>) * B * LineLD<T, N>::value;
-  if (smem > 48 * 1024) {
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(fft_kernel<T, N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+  {
+    cudaError_t e = ensure_smem((const void*)fft_kernel<T, N, B>, smem);
+    if (e != cudaSuccess) return e;
   }
   fft_kernel<T, N, B><<<(unsigned)blocks, B * TPL, smem, st>>>(a);
   return cudaGetLastError();
-}
-
-bool pair_enabled() {
-  static const bool on = !getenv("GF_FFT_NOPAIR");
-  return on;
 }
 
 template <int N, int B>
@@ -710,21 +696,12 @@ cudaError_t launch_pair(const FftArgs& a, cudaStream_t st) {
   const int so = a.axis == 0 ? a.shape_in[1] : a.shape_in[0];
   const int64_t blocks = (int64_t)so * ceil_div(a.shape_in[2], B);
   constexpr size_t smem = sizeof(cx<float>) * B * LineLD<float, N>::value;
-  if (smem > 48 * 1024) {
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(fft_pair_kernel<N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+  {
+    cudaError_t e = ensure_smem((const void*)fft_pair_kernel<N, B>, smem);
+    if (e != cudaSuccess) return e;
   }
   fft_pair_kernel<N, B><<<(unsigned)blocks, B / 2 * (N / 8), smem, st>>>(a);
   return cudaGetLastError();
-}
-
-bool staged_enabled() {
-  static const bool on = !getenv("GF_FFT_NOSTAGE");
-  return on;
 }
 
 template <typename T, int N, int B>
@@ -732,24 +709,11 @@ cudaError_t launch_staged(const FftArgs& a, cudaStream_t st) {
   const int64_t ntiles = ceil_div((int64_t)a.shape_in[0] * a.shape_in[1], B);
   const size_t smem = 128 + sizeof(cx<T>) * ((size_t)2 * B * a.shape_in[2] + (size_t)B * LineLD<T, N>::value);
   if (smem > 200 * 1024) return launch_nb<T, N, B>(a, st);
-  static size_t configured = 0;
-  static int per_sm = 1;
-  if (smem > configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(fft_rows_staged_kernel<T, N, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  static size_t occ_smem = 0;
-  if (occ_smem != smem) {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fft_rows_staged_kernel<T, N, B>, B * (N / 8), smem);
-    per_sm = n > 0 ? n : 1;
-    occ_smem = smem;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = (const void*)fft_rows_staged_kernel<T, N, B>;
+  cudaError_t e = ensure_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = resident_ctas(fn, B * (N / 8), smem);
+  const int sms = sm_count();
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
   fft_rows_staged_kernel<T, N, B><<<(unsigned)grid, B * (N / 8), smem, st>>>(a, ntiles);
   return cudaGetLastError();
@@ -768,11 +732,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
   return fn;
-}
-
-bool tma_enabled() {
-  static const bool on = !getenv("GF_FFT_NOTMA");
-  return on;
 }
 
 // 3-D map over a (s0, s1, s2) complex array in 8-byte units; box of 128 bytes
@@ -812,22 +771,11 @@ cudaError_t launch_tma(const FftArgs& a, cudaStream_t st) {
   const int so = a.axis == 0 ? a.shape_in[1] : a.shape_in[0];
   const int64_t ntiles = (int64_t)so * g.ptiles;
   const size_t smem = 128 + (size_t)3 * N * 128;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fft_cols_tma_kernel<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  static int per_sm = 0;
-  if (!per_sm) {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fft_cols_tma_kernel<T, N>, RB * (N / 8), smem);
-    per_sm = n > 0 ? n : 1;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* fn = (const void*)fft_cols_tma_kernel<T, N>;
+  cudaError_t e = ensure_smem(fn, smem);
+  if (e != cudaSuccess) return e;
+  const int per_sm = resident_ctas(fn, RB * (N / 8), smem);
+  const int sms = sm_count();
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
   fft_cols_tma_kernel<T, N><<<(unsigned)grid, RB * (N / 8), smem, st>>>(tin, tout, a, g, ntiles);
   return cudaGetLastError();
@@ -843,19 +791,17 @@ cudaError_t launch_n(const FftArgs& a, cudaStream_t st) {
   constexpr int B_thr = (256 / TPL) < 1 ? 1 : (256 / TPL) > 32 ? 32 : (256 / TPL);
   constexpr int B_str = (B_row > B_thr ? B_row : B_thr) * TPL > 1024 ? 1024 / TPL : (B_row > B_thr ? B_row : B_thr);
   if constexpr (N >= 64) {
-    if (a.axis == 2 && staged_enabled() && ((int64_t)B_thr * a.shape_in[2] * sizeof(cx<T>)) % 16 == 0 &&
+    if (a.axis == 2 && ((int64_t)B_thr * a.shape_in[2] * sizeof(cx<T>)) % 16 == 0 &&
         ((uintptr_t)a.in & 15) == 0)
       return launch_staged<T, N, B_thr>(a, st);
   }
   if (a.axis == 2) return launch_nb<T, N, B_thr>(a, st);
   if constexpr (N >= 64 && N <= 512) {
-    if (tma_enabled()) {
-      cudaError_t e = launch_tma<T, N>(a, st);
-      if (e != cudaErrorNotSupported) return e;
-    }
+    cudaError_t e = launch_tma<T, N>(a, st);
+    if (e != cudaErrorNotSupported) return e;
   }
   if constexpr (sizeof(T) == 4 && N >= 64 && N <= 512) {
-    if (a.shape_in[2] % 2 == 0 && a.shape_out[2] % 2 == 0 && pair_enabled()) return launch_pair<N, 16>(a, st);
+    if (a.shape_in[2] % 2 == 0 && a.shape_out[2] % 2 == 0) return launch_pair<N, 16>(a, st);
   }
   return launch_nb<T, N, B_str>(a, st);
 }

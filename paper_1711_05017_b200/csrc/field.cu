@@ -61,175 +61,6 @@ __device__ __forceinline__ double exact_u_f(const double* R, const double* dom, 
 }
 
 // ---------------------------------------------------------------------------
-// Fused landscape pass 1: the product Q = C1 V exp(2 pi i w.s) is formed in
-// registers for every retained mode of a z-line and the line is inverse-
-// transformed along z (window-centred input, N2 node outputs) before it ever
-// reaches memory.  A CTA owns a BX x BY tile of (kx, ky) lines so that the
-// rotated corner gathers of neighbouring lines share cache lines; lanes run
-// along each line (coalesced C1 loads and output stores).
-
-struct ZArgs {
-  const void* C1;
-  const void* C2p;
-  const void* px;   // per-axis phase tables exp(2 pi i kappa_a dw_a s_a), complex<T>
-  const void* py;
-  const void* pz;
-  const void* tw;
-  void* out;        // (nkx, w1, N2)
-  int w[3];
-  int N2;
-  int kx0, nkx;
-  double dom[3];
-  double R[9];
-  double mu[3][3];
-  double tie_eps;
-};
-
-template <typename T, int N, int BX, int BY, bool WRAP>
-__global__ void __launch_bounds__(BX * BY * FftShape<N>::TPL) field_zpass_kernel(ZArgs a) {
-  using P4 = typename pair4<T>::type;
-  constexpr int TPL = FftShape<N>::TPL, PT = FftShape<N>::PT, LD = LineLD<T, N>::value, B = BX * BY;
-  extern __shared__ __align__(16) unsigned char zsmem[];
-  cx<T>* buf = reinterpret_cast<cx<T>*>(zsmem);
-  const int tid = threadIdx.x;
-  const int j = tid % TPL, b = tid / TPL;
-  const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
-  const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
-  const int tiles_y = (w1 + BY - 1) / BY;
-  const int kx = a.kx0 + (blockIdx.x / tiles_y) * BX + b / BY;
-  const int ky = (blockIdx.x % tiles_y) * BY + b % BY;
-  const bool live = kx < a.kx0 + a.nkx && ky < w1;
-  const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
-  const cx<T>* __restrict__ C1 = reinterpret_cast<const cx<T>*>(a.C1);
-  const cx<T>* __restrict__ pzt = reinterpret_cast<const cx<T>*>(a.pz);
-  const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
-  const T eps = (T)a.tie_eps;
-
-  cx<T> v[PT];
-  if (live) {
-    const double kapx = kx - hx, kapy = ky - hy;
-    const T ub0 = (T)(hx + a.mu[0][0] * kapx + a.mu[0][1] * kapy);
-    const T ub1 = (T)(hy + a.mu[1][0] * kapx + a.mu[1][1] * kapy);
-    const T ub2 = (T)(hz + a.mu[2][0] * kapx + a.mu[2][1] * kapy);
-    const T mz0 = (T)a.mu[0][2], mz1 = (T)a.mu[1][2], mz2 = (T)a.mu[2][2];
-    const cx<T> pxy = reinterpret_cast<const cx<T>*>(a.px)[kx] * reinterpret_cast<const cx<T>*>(a.py)[ky];
-    const cx<T>* c1row = C1 + ((int64_t)kx * w1 + ky) * w2;
-#pragma unroll
-    for (int r = 0; r < PT; ++r) {
-      const int pos = j + r * TPL;
-      const int m = pos < N / 2 ? pos : pos - N;
-      const int kz = m + hz;
-      cx<T> q = mk<T>(0, 0);
-      if (kz >= 0 && kz < w2) {
-        const T kapz = (T)(kz - hz);
-        T u[3] = {fma(kapz, mz0, ub0), fma(kapz, mz1, ub1), fma(kapz, mz2, ub2)};
-        T fl[3], f[3];
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          fl[ax] = floor(u[ax]);
-          f[ax] = u[ax] - fl[ax];
-        }
-        if (f[0] < eps || f[0] > (T)1 - eps || f[1] < eps || f[1] > (T)1 - eps || f[2] < eps ||
-            f[2] > (T)1 - eps) {
-#pragma unroll
-          for (int ax = 0; ax < 3; ++ax) {
-            if (f[ax] < eps || f[ax] > (T)1 - eps) {
-              double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
-              double fe = floor(ue);
-              fl[ax] = (T)fe;
-              f[ax] = (T)(ue - fe);
-            }
-          }
-        }
-        int ix = (int)fl[0], iy = (int)fl[1], iz = (int)fl[2];
-        bool ok = true;
-        if (WRAP) {
-          ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
-          iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
-          iz = iz < 0 ? iz + w2 : (iz >= w2 ? iz - w2 : iz);
-        } else {
-          ok = (unsigned)(ix + 1) <= (unsigned)w0 && (unsigned)(iy + 1) <= (unsigned)w1 &&
-               (unsigned)(iz + 1) <= (unsigned)w2;
-        }
-        if (ok) {
-          const P4* p = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
-          P4 e00 = ldg_pair(p), e10 = ldg_pair(p + sx), e01 = ldg_pair(p + sy), e11 = ldg_pair(p + sx + sy);
-          const T fu = f[0], fv = f[1], fs = f[2];
-          cx<T> a00 = lerp(mk<T>(e00.x, e00.y), mk<T>(e10.x, e10.y), fu);
-          cx<T> a01 = lerp(mk<T>(e00.z, e00.w), mk<T>(e10.z, e10.w), fu);
-          cx<T> a10 = lerp(mk<T>(e01.x, e01.y), mk<T>(e11.x, e11.y), fu);
-          cx<T> a11 = lerp(mk<T>(e01.z, e01.w), mk<T>(e11.z, e11.w), fu);
-          const cx<T> V = lerp(lerp(a00, a10, fv), lerp(a01, a11, fv), fs);
-          q = c1row[kz] * V * (pxy * pzt[kz]);
-        }
-      }
-      v[r] = q;
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < PT; ++r) v[r] = mk<T>(0, 0);
-  }
-  cx<T>* line = buf + b * LD;
-  fft_line<T, N>(v, line, j, reinterpret_cast<const cx<T>*>(a.tw), +1);
-  if (!live) return;
-  cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out) + ((int64_t)(kx - a.kx0) * w1 + ky) * a.N2;
-#pragma unroll
-  for (int r = 0; r < PT; ++r) out[j + r * TPL] = line[sidx<T>(j + r * TPL)];
-}
-
-template <typename T>
-__global__ void phase_tables_kernel(cx<T>* px, cx<T>* py, cx<T>* pz, int w0, int w1, int w2, double t0, double t1,
-                                    double t2) {
-  const int n = w0 + w1 + w2;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    int ax = i < w0 ? 0 : (i < w0 + w1 ? 1 : 2);
-    int k = i - (ax == 0 ? 0 : (ax == 1 ? w0 : w0 + w1));
-    int h = ax == 0 ? w0 / 2 : (ax == 1 ? w1 / 2 : w2 / 2);
-    double cyc = (ax == 0 ? t0 : (ax == 1 ? t1 : t2)) * (double)(k - h);
-    cyc -= rint(cyc);
-    double sn, cs;
-    sincospi(2.0 * cyc, &sn, &cs);
-    cx<T> v = mk<T>((T)cs, (T)sn);
-    if (ax == 0) px[k] = v;
-    else if (ax == 1) py[k] = v;
-    else pz[k] = v;
-  }
-}
-
-template <typename T, int N, bool WRAP>
-cudaError_t launch_zpass_t(const ZArgs& a, cudaStream_t st) {
-  constexpr int TPL = FftShape<N>::TPL;
-  // 2D line tile: up to 1024 threads, >= 16 lines for fp32 (8 for fp64)
-  constexpr int Bmax = sizeof(T) == 4 ? 16 : 8;
-  constexpr int B = (1024 / TPL) > Bmax ? Bmax : (1024 / TPL);
-  constexpr int BX = B >= 16 ? 4 : (B >= 4 ? 2 : 1);
-  constexpr int BY = B / BX;
-  constexpr size_t smem = sizeof(cx<T>) * B * LineLD<T, N>::value;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(field_zpass_kernel<T, N, BX, BY, WRAP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  const int tiles = (int)(ceil_div(a.nkx, BX) * ceil_div(a.w[1], BY));
-  field_zpass_kernel<T, N, BX, BY, WRAP><<<tiles, B * TPL, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename T, bool WRAP>
-cudaError_t launch_zpass_w(const ZArgs& a, cudaStream_t st) {
-  switch (a.N2) {
-    case 32: return launch_zpass_t<T, 32, WRAP>(a, st);
-    case 64: return launch_zpass_t<T, 64, WRAP>(a, st);
-    case 128: return launch_zpass_t<T, 128, WRAP>(a, st);
-    case 256: return launch_zpass_t<T, 256, WRAP>(a, st);
-    case 512: return launch_zpass_t<T, 512, WRAP>(a, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Brick-ordered product kernel: each CTA owns an 8 x 8 x 8 brick of window
 // modes (2 per thread), so the rotated footprint of a CTA in C2 is a compact
 // rotated brick -- each C2 sector comes from DRAM about once even when the
@@ -459,70 +290,6 @@ int gf_rotate_product(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   return gf_rotate_product_planes(h1, h2, wrap, domega, R, s, precision, 0, -1, out_dev, stream);
 }
 
-int gf_field_zpass(uint64_t h1, uint64_t h2, int wrap, const double* domega, int n2, const double* R,
-                   const double* s, int precision, int kx0, int nkx, void* out_dev, void* stream) {
-  GF_CHECK(domega && R && s && out_dev, GF_EINVAL, "null argument");
-  GF_CHECK(n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256 || n2 == 512, GF_EINVAL,
-           "fused pass supports N2 in {32..512}");
-  cudaStream_t st = (cudaStream_t)stream;
-  ZArgs a = {};
-  const void* c1 = nullptr;
-  const void* c2 = nullptr;
-  int dim = 0;
-  int rc = window_operands(h1, h2, wrap, precision, st, &c1, &c2, a.w, &dim);
-  if (rc) return rc;
-  GF_CHECK(dim == 3 && c1 != nullptr, GF_EINVAL, "fused pass needs two 3D windows");
-  GF_CHECK(a.w[2] <= n2, GF_EINVAL, "window longer than N2");
-  if (nkx < 0) {
-    kx0 = 0;
-    nkx = a.w[0];
-  }
-  GF_CHECK(kx0 >= 0 && kx0 + nkx <= a.w[0], GF_EINVAL, "plane range outside the window");
-  if (nkx == 0) return 0;
-  a.C1 = c1;
-  a.C2p = c2;
-  a.out = out_dev;
-  a.N2 = n2;
-  a.kx0 = kx0;
-  a.nkx = nkx;
-  for (int k = 0; k < 3; ++k) a.dom[k] = domega[k];
-  for (int k = 0; k < 9; ++k) a.R[k] = R[k];
-  for (int i = 0; i < 3; ++i)
-    for (int jj = 0; jj < 3; ++jj) a.mu[i][jj] = -R[jj * 3 + i] * (domega[jj] / domega[i]);
-  double umax = 0.0;
-  for (int ax = 0; ax < 3; ++ax) {
-    double v = a.w[ax] / 2;
-    for (int b = 0; b < 3; ++b) v += (a.dom[b] / a.dom[ax]) * (a.w[b] / 2 + 1);
-    umax = v > umax ? v : umax;
-  }
-  double eps = 8.0 * ldexp(umax, precision == 32 ? -23 : -52);
-  double floor_eps = precision == 32 ? 1e-4 : 1e-9;
-  a.tie_eps = eps > floor_eps ? eps : floor_eps;
-  // phase tables (per call; tiny) and twiddles (cached)
-  const size_t esz = precision == 32 ? 8 : 16;
-  void* tabs = nullptr;
-  GF_CUDA(cudaMallocAsync(&tabs, esz * (a.w[0] + a.w[1] + a.w[2]), st));
-  a.px = tabs;
-  a.py = (char*)tabs + esz * a.w[0];
-  a.pz = (char*)tabs + esz * (a.w[0] + a.w[1]);
-  const double t0 = domega[0] * s[0], t1 = domega[1] * s[1], t2 = domega[2] * s[2];
-  if (precision == 32)
-    phase_tables_kernel<float><<<4, 256, 0, st>>>((cx<float>*)a.px, (cx<float>*)a.py, (cx<float>*)a.pz, a.w[0], a.w[1],
-                                                 a.w[2], t0, t1, t2);
-  else
-    phase_tables_kernel<double><<<4, 256, 0, st>>>((cx<double>*)a.px, (cx<double>*)a.py, (cx<double>*)a.pz, a.w[0],
-                                                  a.w[1], a.w[2], t0, t1, t2);
-  GF_CUDA(cudaGetLastError());
-  a.tw = twiddles(precision, n2, +1, st);
-  GF_CHECK(a.tw != nullptr, GF_ENOMEM, "twiddle table allocation failed");
-  cudaError_t e;
-  if (precision == 32) e = wrap ? launch_zpass_w<float, true>(a, st) : launch_zpass_w<float, false>(a, st);
-  else e = wrap ? launch_zpass_w<double, true>(a, st) : launch_zpass_w<double, false>(a, st);
-  GF_CUDA(e);
-  GF_CUDA(cudaFreeAsync(tabs, st));
-  return 0;
-}
-
 int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double* domega, const int32_t* dims, const double* R,
                    const double* s, double scale, int precision, void* work_dev, void* work2_dev, void* out_dev,
                    void* stream) {
@@ -532,17 +299,8 @@ int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double* domega, con
   int w[3], dim;
   int rc = window_operands(h1, h2, wrap, precision, (cudaStream_t)stream, &c1, &c2, w, &dim);
   if (rc) return rc;
-  const int n2 = dim == 3 ? dims[2] : dims[1];
-  static const int fuse_env = getenv("GF_FIELD_FUSED") ? atoi(getenv("GF_FIELD_FUSED")) : 0;
-  const bool fused = fuse_env && dim == 3 && (n2 == 32 || n2 == 64 || n2 == 128 || n2 == 256 || n2 == 512);
-  if (fused) {
-    // pass 1 fused with the product: (w0, w1, N2) straight into work2
-    rc = gf_field_zpass(h1, h2, wrap, domega, n2, R, s, precision, 0, -1, work2_dev, stream);
-    if (rc) return rc;
-  } else {
-    rc = gf_rotate_product(h1, h2, wrap, domega, R, s, precision, work_dev, stream);
-    if (rc) return rc;
-  }
+  rc = gf_rotate_product(h1, h2, wrap, domega, R, s, precision, work_dev, stream);
+  if (rc) return rc;
   // three pruned inverse passes: window-centred in, node order out
   int32_t N[3] = {dim == 3 ? dims[0] : 1, dim == 3 ? dims[1] : dims[0], dim == 3 ? dims[2] : dims[1]};
   int32_t W[3] = {dim == 3 ? w[0] : 1, dim == 3 ? w[1] : w[0], dim == 3 ? w[2] : w[1]};
@@ -550,10 +308,8 @@ int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double* domega, con
   int32_t sh1[3] = {W[0], W[1], N[2]};
   int32_t sh2[3] = {W[0], N[1], N[2]};
   int32_t sh3[3] = {N[0], N[1], N[2]};
-  if (!fused) {
-    rc = gf_fft_pass(precision, work_dev, work2_dev, sh0, sh1, 2, N[2], 1, 0, 1, 0.0, 0.0, 1.0, stream);
-    if (rc) return rc;
-  }
+  rc = gf_fft_pass(precision, work_dev, work2_dev, sh0, sh1, 2, N[2], 1, 0, 1, 0.0, 0.0, 1.0, stream);
+  if (rc) return rc;
   if (dim == 3) {
     rc = gf_fft_pass(precision, work2_dev, work_dev, sh1, sh2, 1, N[1], 1, 0, 1, 0.0, 0.0, 1.0, stream);
     if (rc) return rc;

@@ -30,6 +30,17 @@ from .energy import Configuration, EnergyEval, evaluate
 
 __all__ = ["HapticSession"]
 
+_SPIN_S = 150e-6  # spin only the last 150 us of a frame's slack (sleep wake-up jitter)
+
+
+def _rt_runtime_us():
+    """The kernel's real-time budget per second (-1: unlimited), or None."""
+    try:
+        with open("/proc/sys/kernel/sched_rt_runtime_us") as fh:
+            return int(fh.read().strip())
+    except (OSError, ValueError):
+        return None
+
 
 def _enter_realtime():
     """Pin the calling thread to the highest-numbered core it may use and
@@ -111,7 +122,7 @@ class HapticSession:
                 return True
         return False  # every trial climbed: hold the pose
 
-    def run(self, rotations, translations, rate_hz=1000.0, resident=True, realtime=True):
+    def run(self, rotations, translations, rate_hz=1000.0, resident=True, realtime=True, max_sms=0):
         """Pace a pose trajectory at `rate_hz`; returns latency stats and misses.
 
         resident=True serves the frames from a persistent query grid
@@ -121,11 +132,12 @@ class HapticSession:
         pinned to one host core at SCHED_FIFO priority (restored afterwards;
         skipped when the OS refuses, reported as "realtime": False).  Measured
         on the B200 box: unpinned, 1-2 frames per 1000 stall for 1-5 ms while
-        the thread is descheduled; pinned at SCHED_FIFO, none."""
+        the thread is descheduled; pinned at SCHED_FIFO, none.  `max_sms`
+        is handed to the resident grid (see backend.HapticServer)."""
         if resident:
             from .energy import haptic_session
 
-            with haptic_session(self.fixed, self.moving, self.modes):
+            with haptic_session(self.fixed, self.moving, self.modes, max_sms=max_sms):
                 return self._run(rotations, translations, rate_hz, realtime)
         return self._run(rotations, translations, rate_hz, realtime)
 
@@ -147,9 +159,14 @@ class HapticSession:
                 gc.enable()
 
     def _paced(self, rotations, translations, period, rate_hz):
-        lat, misses = [], 0
+        """Servo pacing: sleep through most of the slack, spin only the last
+        `_SPIN_S`.  A SCHED_FIFO thread that busy-waits the whole period uses
+        100 % of its core and hits the kernel's real-time throttle
+        (sched_rt_runtime_us, 950 ms of every 1 s by default): it is then
+        descheduled for ~50 ms -- the 46 ms frame of the round-1 C5 run."""
+        lat, misses, late = [], 0, []
         t_next = time.perf_counter()
-        for R, t in zip(rotations, translations):
+        for i, (R, t) in enumerate(zip(rotations, translations)):
             self.rotation, self.translation = np.asarray(R), np.asarray(t)
             t0 = time.perf_counter()
             self.eval_current()
@@ -157,11 +174,17 @@ class HapticSession:
             lat.append(dt * 1e6)
             if dt > period:
                 misses += 1
+                if len(late) < 16:
+                    late.append({"frame": i, "us": dt * 1e6, "start_lag_us": (t0 - t_next) * 1e6})
             t_next += period
-            while time.perf_counter() < t_next:  # servo pacing (busy wait: haptic threads spin)
+            slack = t_next - time.perf_counter()
+            if slack > _SPIN_S:
+                time.sleep(slack - _SPIN_S)
+            while time.perf_counter() < t_next:
                 pass
         worst = max(range(len(lat)), key=lat.__getitem__) if lat else -1
         lat.sort()
         pct = lambda p: lat[min(len(lat) - 1, int(p * len(lat)))]  # noqa: E731  (cli.py:357-361)
         return {"frames": len(lat), "p50_us": statistics.median(lat), "p95_us": pct(0.95), "p99_us": pct(0.99),
-                "max_us": lat[-1], "max_frame": worst, "deadline_misses": misses, "rate_hz": rate_hz}
+                "max_us": lat[-1], "max_frame": worst, "deadline_misses": misses, "missed": late,
+                "rate_hz": rate_hz, "rt_runtime_us": _rt_runtime_us()}

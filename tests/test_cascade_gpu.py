@@ -150,10 +150,37 @@ def test_haptic_server_2d_fp64_and_idle_timeout(be):
     with pytest.raises(EngineError, match="idle timeout"):
         be.check(be.LIB.gf_server_query(srv.id, *[be.dptr(np.ascontiguousarray(x)) for x in
                                                   (np.eye(2), np.zeros(2), np.zeros(14))]))
+    # the operator call on that pair is still served: it retires the exited
+    # server and falls back to one launch per query (same result)
+    assert srv.key in be._servers
+    late = be.cascade(W1, W2, False, dom, 0.3, poses[1][0], poses[1][1], c, precision="fp64")
+    np.testing.assert_array_equal(late, want[1])
+    assert srv.key not in be._servers
     srv.stop()
     with be.HapticServer(W1, W2, False, dom, 0.3, c, precision="fp64"):
         again = be.cascade(W1, W2, False, dom, 0.3, poses[0][0], poses[0][1], c, precision="fp64")
     np.testing.assert_array_equal(again, want[0])
+
+
+@pytest.mark.parametrize("max_sms", [1, 37, 100])
+def test_haptic_server_sm_budget(be, max_sms):
+    """A server held to a subset of the SMs answers within the
+    parity tolerance of the oracle (its mode split differs from the launch
+    path, so not bit for bit), repeatably."""
+    rng = np.random.default_rng(23 + max_sms)
+    w = 64
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom, dcell, c = (0.05,) * 3, 0.3, rng.normal(size=3)
+    poses = [(random_rotation(rng), rng.uniform(-1, 1, 3)) for _ in range(3)]
+    with be.HapticServer(W1, W2, False, dom, dcell, c, max_sms=max_sms):
+        got = [be.cascade(W1, W2, False, dom, dcell, R, t, c) for R, t in poses]
+        again = [be.cascade(W1, W2, False, dom, dcell, R, t, c) for R, t in poses]
+    for g, a_, (R, t) in zip(got, again, poses):
+        np.testing.assert_array_equal(g, a_)
+        want = oracle.cascade(C1, C2, False, dom, dcell, R, t, c)
+        l1 = oracle.cascade_term_scales(C1, C2, False, dom, dcell, R, t, c)
+        assert np.all(parity_tol(g, want, l1, 1e-4))
 
 
 @pytest.mark.parametrize("w,wrap", [(48, False), (64, True), (96, False)])
