@@ -593,3 +593,53 @@ def raycast_inside(triangles, P, seed=0):
         out[todo[done]] = (count[done] % 2) == 1
         todo = todo[graze]
     return out
+
+
+def _interp_values(C, u, wrap):
+    """V only of interp_window (no index gradient): the multilinear sample."""
+    d = C.ndim
+    dims = C.shape
+    flat = C.ravel()
+    i0 = np.floor(u).astype(np.int64)
+    f = u - i0
+    V = np.zeros(len(u), dtype=np.complex128)
+    for corner in itertools.product((0, 1), repeat=d):
+        lin = np.zeros(len(u), dtype=np.int64)
+        ok = np.ones(len(u), dtype=bool)
+        wgt = np.ones(len(u))
+        for a in range(d):
+            ia = i0[:, a] + corner[a]
+            if wrap:
+                ia = ia % dims[a]
+            else:
+                ok &= (ia >= 0) & (ia < dims[a])
+                ia = np.clip(ia, 0, dims[a] - 1)
+            lin = lin * dims[a] + ia
+            wgt = wgt * (f[:, a] if corner[a] else 1.0 - f[:, a])
+        V += np.where(ok, wgt * flat[lin], 0.0)
+    return V
+
+
+def score_field_scale(C1, C2, wrap, dims, spacing, R, stride=1, chunk=1 << 22):
+    """dcell * sum_w |C1(w) V(w)|: the L1 floor of the landscape parity
+    tolerance (the translation phase has unit modulus, so it is the same at
+    every voxel; energy.py:309-344).  Modes are taken in x-plane chunks so a
+    512^3 window stays within a few GB; stride > 1 estimates the sum from
+    every stride-th mode per axis (times stride^d)."""
+    C1 = np.asarray(C1)
+    window = C1.shape
+    d = len(window)
+    dom = np.asarray([1.0 / (n * spacing) for n in dims])
+    half = np.asarray([w // 2 for w in window])
+    ks = [np.arange(0, w, stride) for w in window]
+    total = 0.0
+    per = max(1, chunk // int(np.prod([len(k) for k in ks[1:]])))
+    for x0 in range(0, len(ks[0]), per):
+        kk = [ks[0][x0:x0 + per]] + ks[1:]
+        mesh = np.meshgrid(*kk, indexing="ij")
+        K = np.stack([m.ravel() for m in mesh], axis=1)
+        W = (K - half) * dom
+        V = _interp_values(C2, -(W @ R) / dom + half, wrap)
+        total += float(np.sum(np.abs(C1[tuple(mesh)].ravel() * V)))
+    dcell = 1.0 / (float(np.prod(dims)) * spacing ** d)
+    return dcell * total * stride ** d
