@@ -19,13 +19,22 @@ sigma_theta = 0.5 deg; t sliding along z with sigma_t = h/4), issued as
   cpu_baseline  the reference's own compiled kernel (_core.cascade_3d built
           from /root/reference into oracle/_ref) on the same windows, 1 core
           (it is single-threaded by design, backend.py:153-164).
+  parity  per stage, max |new - ref| / (1e-4 max(|ref|, L1)) (<= 1 passes,
+          BASELINE.md section 2) and the plain relative error, against the
+          reference kernel (oracle/_ref) or the oracle restatement.
+  stages  the other BASELINE configs on their stated inputs (C1 peg-in-hole
+          64^3 trajectory, C2 on real assets, C3 gear-pair 10^6-pose sweep,
+          C4 512^3 landscape of real spectra, C5 bolt-nut 1 kHz trajectory,
+          stage-1 density and stage-2 window), compact.
 
 --impl reference runs the reference kernel with every host core (a thread
 pool over poses; _core.cascade_3d releases the GIL) on the same config.
 
-Multi-GPU: the single haptic query does not shard:
-`--gpus N` runs N independent replicas, one per rank, and value/e2e are the
-whole-job totals (max-over-ranks time).
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself
+under torch.distributed.run with N ranks.  The single haptic query does not
+shard: N independent replicas, whole-job totals
+(max-over-ranks time).  The C3 sweep shards its 10^6 poses by rank and the
+C4 landscape is slab-decomposed across ranks (parallel.score_field_slab).
 """
 
 from __future__ import annotations
@@ -33,6 +42,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -50,6 +60,19 @@ W = 2 * K_TRUNC
 DOMAIN = 3.46  # grid_for_pair domain of the C1/C2 peg pair
 QUERIES_PER_STEP = 1000
 SEED = 20260814
+METRIC = "pose queries/sec (energy+force+torque) at K=32, 128^3, single-query loop"
+CONFIG = {"workload": "C2 haptic query loop: 128^3 grid, K=32 (w=64, m'=262144), 1000 serial single queries per step",
+          "grid": GRID_N, "K": K_TRUNC, "w": W, "m_prime": W ** 3, "queries_per_step": QUERIES_PER_STEP,
+          "poses": "jittered insertion path, rng seed 20260814",
+          "l2": "flushed between steps (256 MiB write); windows L2-resident within a step as in a live haptic loop",
+          "parallelism": "replicas: one independent haptic loop per GPU"}
+
+
+def r4(x):
+    """Compact float for the JSON line (4 significant digits)."""
+    if x is None or isinstance(x, (bool, int, str)):
+        return x
+    return float(f"{float(x):.4g}")
 
 
 def synthetic_windows(w, seed=SEED):
@@ -157,19 +180,32 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ---------------------------------------------------------------------------
+# process topology
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: re-launch this script with N ranks
+    (torch.distributed.run, loopback rendezvous) and return its exit code."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def dist_setup():
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
     return world, rank, local
 
 
@@ -199,20 +235,21 @@ def barrier(world):
 
 def cmd_bench_poses(n, span, seed=0):
     rng = np.random.default_rng(seed)
-    Rs, ts = [], []
-    for _ in range(n):
-        w, x, y, z = rng.normal(size=4)
-        nrm = np.sqrt(w * w + x * x + y * y + z * z)
-        w, x, y, z = w / nrm, x / nrm, y / nrm, z / nrm
-        Rs.append([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
-                   [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
-                   [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
-        ts.append(rng.uniform(-span, span, 3))
-    return np.asarray(Rs), np.asarray(ts)
+    q = np.empty((n, 4))
+    t = np.empty((n, 3))
+    for i in range(n):  # the reference's draw order: 4 normals, then 3 uniforms, per pose
+        q[i] = rng.normal(size=4)
+        t[i] = rng.uniform(-span, span, 3)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    R = np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)], -1),
+                  np.stack([2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)], -1),
+                  np.stack([2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)], -1)], 1)
+    return R, t
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (the reference's compiled kernel, oracle/_ref)
+# CPU reference (the reference's compiled kernel, oracle/_ref) and parity
 
 
 def reference_core():
@@ -224,17 +261,45 @@ def reference_core():
     return core
 
 
-def cpu_reference_rate(C1, C2, Rs, t_eff, threads, budget_s):
+def ref_cascade(C1, C2, wrap, dom, dcell, R, t_eff, c):
+    core = reference_core()
+    return np.asarray(core.cascade_3d(np.ascontiguousarray(C1), np.ascontiguousarray(C2), bool(wrap), *dom, dcell,
+                                      np.ascontiguousarray(R), np.ascontiguousarray(t_eff), np.ascontiguousarray(c)))
+
+
+def parity_entry(got, want, l1, against):
+    """got/want complex [n, 7] (or [n]) arrays; l1 the per-output term scales."""
+    got, want, l1 = np.asarray(got), np.asarray(want), np.asarray(l1)
+    den = 1e-4 * np.maximum(np.abs(want), l1)
+    return {"err_tol": r4(np.max(np.abs(got - want) / den)),
+            "rel": r4(np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-300)),
+            "n": int(want.shape[0]) if want.ndim > 1 else int(want.size), "vs": against}
+
+
+def parity_of_poses(C1, C2, wrap, dom, dcell, c, Rs, t_effs, got, threads=8):
+    """Reference kernel (oracle/_ref) on the same windows/poses, in a thread pool."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        want = list(pool.map(lambda i: ref_cascade(C1, C2, wrap, dom, dcell, Rs[i], t_effs[i], c), range(len(Rs))))
+        l1 = list(pool.map(lambda i: oracle.cascade_term_scales(C1, C2, wrap, dom, dcell, Rs[i], t_effs[i], c),
+                           range(len(Rs))))
+    return parity_entry(np.asarray(got), np.asarray(want), np.asarray(l1), "oracle/_ref _core.cascade_3d")
+
+
+def cpu_reference_rate(C1, C2, Rs, t_eff, threads, budget_s, wrap=False, consts=None):
     """Queries/s of _core.cascade_3d on `threads` host threads for ~budget_s."""
     from concurrent.futures import ThreadPoolExecutor
 
     core = reference_core()
-    _, center, dom, dcell = grid_params()
+    _, center, dom, dcell = consts or grid_params()
     C1 = np.ascontiguousarray(C1)
     C2 = np.ascontiguousarray(C2)
 
     def one(i):
-        return core.cascade_3d(C1, C2, False, dom[0], dom[1], dom[2], dcell, np.ascontiguousarray(Rs[i]),
+        return core.cascade_3d(C1, C2, bool(wrap), dom[0], dom[1], dom[2], dcell, np.ascontiguousarray(Rs[i]),
                                np.ascontiguousarray(t_eff[i]), center)
 
     one(0)  # warm
@@ -273,12 +338,10 @@ def run_reference_arm(args):
     total = time.perf_counter() - t_all
     value = float(np.sum(samples) / total)
     line = {
-        "impl": "reference", "metric": "pose queries/sec (energy+force+torque) at K=32, 128^3, single-query loop",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 haptic query loop: 128^3 grid, K=32 (w=64, m'=262144)",
-                   "grid": GRID_N, "K": K_TRUNC, "w": W, "m_prime": W ** 3},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": CONFIG,
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "reference",
                          "sample": f"{int(np.mean(samples))} poses of the trajectory per step, "
                                    f"_core.cascade_3d on a {threads}-thread pool"},
@@ -347,46 +410,28 @@ def run_engine(args):
     # query; the one-shot launch path is reported beside it.
     Re, _, te = trajectory(args.e2e_queries + 50, SEED + 7 + rank)
 
-    def e2e_loop():
+    def e2e_loop(precision):
         lat = []
         for i in range(50):
-            backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision=prec)
+            backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision=precision)
         barrier(world)
         t0 = time.perf_counter()
         for i in range(50, 50 + args.e2e_queries):
             q0 = time.perf_counter_ns()
-            backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision=prec)
+            backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision=precision)
             lat.append((time.perf_counter_ns() - q0) / 1e3)
         dt = time.perf_counter() - t0
         barrier(world)
         return sorted(lat), max_over_ranks(dt, world)
 
-    # headline: the haptic-session path (energy.haptic_session / backend.HapticServer:
-    # a resident query grid, pose in and result out through self-tagged
-    # host-mapped slots); the one-shot launch per call is reported beside it
     with backend.HapticServer(W1, W2, False, dom, dcell, center, precision=prec):
-        lat, e2e_s = e2e_loop()
-    lat1, dt1 = e2e_loop()  # no server: one single-query kernel launch per call
+        lat, e2e_s = e2e_loop(prec)
+    lat1, dt1 = e2e_loop(prec)  # no server: one single-query kernel launch per call
     e2e_value = args.e2e_queries * world / e2e_s
-
-    # the float64 engine (the reference's own tolerances) on the same loop, for reference
-    fp64_mode = None
-    if prec == "fp32":
-        def e2e64():
-            lat64 = []
-            for i in range(50):
-                backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision="fp64")
-            for i in range(50, 50 + args.e2e_queries):
-                q0 = time.perf_counter_ns()
-                backend.cascade(W1, W2, False, dom, dcell, Re[i], te[i], center, precision="fp64")
-                lat64.append((time.perf_counter_ns() - q0) / 1e3)
-            return sorted(lat64)
-
+    lat64 = None
+    if prec == "fp32":  # the float64 engine (the reference's own tolerances) in the same session loop
         with backend.HapticServer(W1, W2, False, dom, dcell, center, precision="fp64"):
-            l64 = e2e64()
-        fp64_mode = {"e2e_p50_us": statistics.median(l64), "e2e_p99_us": l64[min(len(l64) - 1, int(0.99 * len(l64)))],
-                     "e2e_queries_per_s": 1e6 / float(np.mean(l64)),
-                     "note": "same session loop in the float64 engine (reference tolerances 1e-9..1e-12)"}
+            lat64, _ = e2e_loop("fp64")
 
     def pct(xs, p):
         return xs[min(len(xs) - 1, int(p * len(xs)))]
@@ -396,11 +441,20 @@ def run_engine(args):
 
     peak = ctypes.c_double(0.0)
     _lib.check(_lib.LIB.gf_measure_fma_peak(64 if prec == "fp64" else 32, ctypes.byref(peak)))
+    peak64 = ctypes.c_double(0.0)
+    _lib.check(_lib.LIB.gf_measure_fma_peak(64, ctypes.byref(peak64)))
     live = live_fraction(Rs, W)
     flops = 240.0 * live * W ** 3
     achieved = flops / (kernel_us * 1e-6) / 1e12
 
-    stages = {} if args.no_stages else measure_stages(args, rank, world, peak.value)
+    # ---- parity of the timed loop's own outputs against the reference kernel
+    parity = {}
+    if rank == 0 and not args.no_cpu:
+        idx = np.linspace(args.warmup * QUERIES_PER_STEP, n_total - 1, 6).astype(int)
+        got = out[idx].cpu().numpy().view(np.complex128)
+        parity["C2_loop"] = parity_of_poses(C1, C2, False, dom, dcell, center, Rs[idx], t_eff[idx], got)
+
+    stages = {} if args.no_stages else measure_stages(args, rank, world, peak.value, peak64.value, parity)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -411,40 +465,32 @@ def run_engine(args):
 
     if rank == 0:
         line = {
-            "metric": "pose queries/sec (energy+force+torque) at K=32, 128^3, single-query loop",
-            "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
-            "config": {"workload": "C2 haptic query loop: 128^3 grid, K=32 (w=64, m'=262144), "
-                                   "1000 serial single-query launches per step",
-                       "grid": GRID_N, "K": K_TRUNC, "w": W, "m_prime": W ** 3,
-                       "queries_per_step": QUERIES_PER_STEP, "parallelism": f"replicas x{world}",
-                       "l2": "flushed between steps (256 MiB write); windows L2-resident within a step "
-                             "as in a live haptic loop"},
-            "latency_us": {"kernel_mean": kernel_us, "e2e_p50": statistics.median(lat), "e2e_p95": pct(lat, 0.95),
-                           "e2e_p99": pct(lat, 0.99), "launch_path_p50": statistics.median(lat1),
-                           "launch_path_p99": pct(lat1, 0.99), "definition": "cli.py:357-361"},
+            "config": CONFIG,
             "e2e": {"value": e2e_value, "unit": "queries/s",
                     "h2d_bytes_per_step": QUERIES_PER_STEP * 25 * 8, "d2h_bytes_per_step": QUERIES_PER_STEP * 28 * 8,
-                    "step": f"{QUERIES_PER_STEP} serial queries",
-                    "path": "backend.cascade (host R, t_eff in -> host complex128[7] out) inside a haptic session "
-                            "(backend.HapticServer): 25 self-tagged 8-byte request slots read by the GPU from "
-                            "pinned host memory, 28 result slots written back; no launch per query",
-                    "launch_path_value": args.e2e_queries * world / dt1,
-                    "launch_path": "same call without a session: one single-query kernel launch per call"},
-            "roofline": {"bound": "fp32" if prec == "fp32" else "fp64", "achieved": achieved,
-                         "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value,
-                         "traffic": _traffic("cascade3d_single_kernel"),
-                         "traffic_unit": "bytes per launch (DRAM read+write, ncu capture; windows stay L2-resident)",
-                         "work": f"240 flops x live modes ({live:.3f} x {W ** 3}) per launch",
+                    "path": "backend.cascade (host R, t_eff -> host complex128[7]) in a haptic session "
+                            "(backend.HapticServer): 25 self-tagged request slots read from pinned host memory, 28 "
+                            "result slots written back, no launch per query",
+                    "launch_path_value": r4(args.e2e_queries * world / dt1)},
+            "roofline": {"bound": "fp32" if prec == "fp32" else "fp64", "achieved": achieved, "peak": peak.value,
+                         "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": _traffic("cascade3d_single_kernel"),
+                         "work": f"240 flop x live modes ({live:.3f} x {W ** 3}) per launch",
                          "peak_source": "FMA-chain kernel measured in this run (gf_measure_fma_peak)"},
             "cpu_baseline": cpu,
-            "fp64_engine": fp64_mode,
             "gpu_launches": QUERIES_PER_STEP * args.steps,
             "clocks": clk.summary(),
+            "latency_us": {"kernel_mean": r4(kernel_us), "e2e_p50": r4(statistics.median(lat)),
+                           "e2e_p99": r4(pct(lat, 0.99)), "launch_p50": r4(statistics.median(lat1)),
+                           "launch_p99": r4(pct(lat1, 0.99)),
+                           "fp64_e2e_p50": r4(statistics.median(lat64)) if lat64 else None},
+            "parity": parity,
             "stages": stages,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, separators=(",", ":")), flush=True)
+    barrier(world)
     if world > 1:
         import torch.distributed as dist
 
@@ -453,33 +499,25 @@ def run_engine(args):
 
 
 # ---------------------------------------------------------------------------
-# secondary stages (extra keys; the headline metric is the haptic loop above)
+# secondary stages: the other BASELINE configs on their stated inputs
 
 
 def _peaks():
-    import json as _json
-
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return _json.load(fh)
+            return json.load(fh)
     except OSError:
         return {"hbm_gbs": 6650.0, "note": "fallback (B200_PROFILING.md)"}
 
 
 def _traffic(kernel):
     """Per-launch DRAM bytes of `kernel` from the committed ncu capture summary
-    (profiles/r01_traffic.json), or None."""
+    (profiles/traffic.json), or None."""
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             return json.load(fh)[kernel]["bytes"]
     except (OSError, KeyError, ValueError):
         return None
-
-
-def _field_traffic():
-    parts = [_traffic(k) for k in ("product_brick_kernel", "fft_rows_staged_kernel", "fft_cols_tma_kernel",
-                                   "fft_cols_tma_kernel")]
-    return None if None in parts else sum(parts)
 
 
 def _time_ms(fn, reps=3):
@@ -500,7 +538,7 @@ def _time_ms(fn, reps=3):
 
 
 class _Asset:
-    """Minimal PartAsset stand-in holding a device window (synthetic inputs)."""
+    """Minimal PartAsset stand-in holding a device window built on the GPU."""
 
     def __init__(self, grid, win, wrap):
         self.grid, self._win, self._wrap = grid, win, wrap
@@ -512,293 +550,423 @@ class _Asset:
         return int(np.prod(self._win.shape))
 
 
-def measure_stages(args, rank, world, fp32_peak):
+def _gpu_windows(scene, n, w, world, rank):
+    """GPU density (node slabs across ranks when world > 1) and the centred
+    w^3 windows of both parts (spectral.forward_window); returns the two
+    device windows, the grid and the density seconds."""
     import torch
 
-    import oracle  # the stages' cpu_baseline legs only (numpy restatements timed on the host)
-    from paper_1711_05017_b200 import backend, parallel, scenes
-    from paper_1711_05017_b200.descriptor import ComplexField, SampleGrid, affinity_field
-    from paper_1711_05017_b200.energy import score_field_device
+    from paper_1711_05017_b200 import backend, parallel
+    from paper_1711_05017_b200.descriptor import affinity_field
     from paper_1711_05017_b200.spectral import forward_window
 
-    hbm = float(_peaks()["hbm_gbs"])
+    sc = scenes_mod().get_scene(scene)
+    g = sc.grid(n)
+    wins, dens_s = [], 0.0
+    for solid in (sc.fixed, sc.moving):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world > 1:
+            f = parallel.affinity_field_slab(solid, g, sc.kernel)
+        else:
+            f = affinity_field(solid, g, sc.kernel)
+        torch.cuda.synchronize()
+        dens_s += time.perf_counter() - t0
+        wins.append(backend.DeviceWindow(forward_window(f, w)))
+        del f
+    torch.cuda.empty_cache()
+    return wins[0], wins[1], g, dens_s
+
+
+def scenes_mod():
+    from paper_1711_05017_b200 import scenes
+
+    return scenes
+
+
+def measure_stages(args, rank, world, fp32_peak, fp64_peak, parity):
+    import torch
+
     out = {}
-    dev = torch.device("cuda", torch.cuda.current_device())
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(SEED + rank)
+    lead = rank == 0
+    cpu_ok = lead and not args.no_cpu
+    if lead:
+        out.update(stage_trajectories(args, parity, cpu_ok))
+    barrier(world)
+    out["C3"] = stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok)
+    torch.cuda.empty_cache()
+    barrier(world)
+    out["C4"] = stage_field(args, rank, world, parity, cpu_ok)
+    torch.cuda.empty_cache()
+    barrier(world)
+    if lead:
+        out["C5"] = stage_haptic(args, parity, cpu_ok)
+        out["W"] = stage_window(args, parity, cpu_ok)
+        out["D"] = stage_density(args, fp64_peak, parity, cpu_ok)
+    barrier(world)
+    return out
 
-    # --- C1: the reference's own CPU case, end to end on real assets: peg-in-hole 64^3, K=16
-    # (m' = 32^3), GPU density -> spectra -> windows, then a 1000-pose insertion trajectory
-    # through the public evaluate(); the reference kernel runs the same windows and poses
-    from paper_1711_05017_b200.energy import Configuration, evaluate
 
-    sc1 = scenes.get_scene("peg_in_hole")
-    m1 = 32 ** 3
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    p1, p2 = sc1.build_assets(64, m_prime=m1)
-    w1c, w1wrap = p1.window(m1)
-    w2c, _ = p2.window(m1)
-    torch.cuda.synchronize()
-    pre_ms = (time.perf_counter() - t0) * 1e3
-    n_traj = 1000
-    zs = np.linspace(0.6, 0.0, n_traj)  # from clear of the block (peg bottom above its top) to seated
-    cfgs = [Configuration(np.eye(3), np.array([0.0, 0.0, z])) for z in zs]
-    from paper_1711_05017_b200.energy import haptic_session
+def stage_trajectories(args, parity, cpu_ok):
+    """C1 (the reference's CPU case) and C2 on real GPU-built assets, through
+    the public evaluate() inside a haptic session; parity vs the reference
+    kernel on the very windows the engine uses."""
+    import torch
 
-    def run_traj():
-        for cfg in cfgs[:20]:
-            evaluate(p1, p2, cfg, m1)
-        lat, rows = [], []
+    from paper_1711_05017_b200 import backend
+    from paper_1711_05017_b200.energy import Configuration, evaluate, haptic_session
+
+    res = {}
+    for key, scene, n, side, npose in (("C1", "peg_in_hole", 64, 32, 1000), ("C2", "peg_in_hole_lowclear", 128, 64,
+                                                                              2000)):
+        sc = scenes_mod().get_scene(scene)
+        m = side ** 3
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for cfg in cfgs:
-            q0 = time.perf_counter_ns()
-            ev = evaluate(p1, p2, cfg, m1)
-            lat.append((time.perf_counter_ns() - q0) / 1e3)
-            rows.append(np.concatenate([[ev.energy], ev.force, ev.torque]))
-        dt = time.perf_counter() - t0
+        a1, a2 = sc.build_assets(n, m_prime=m)
+        (w1, wrap), (w2, _) = a1.window(m), a2.window(m)
+        torch.cuda.synchronize()
+        pre_ms = (time.perf_counter() - t0) * 1e3
+        if key == "C1":  # insertion trajectory: from clear of the block to seated
+            cfgs = [Configuration(np.eye(3), np.array([0.0, 0.0, z])) for z in np.linspace(0.6, 0.0, npose)]
+        else:  # the headline's jittered path
+            Rj, tj, _ = trajectory(npose, SEED + 11)
+            cfgs = [Configuration(R, t) for R, t in zip(Rj, tj)]
+        with haptic_session(a1, a2, m):
+            for cfg in cfgs[:50]:
+                evaluate(a1, a2, cfg, m)
+            lat, rows = [], []
+            t0 = time.perf_counter()
+            for cfg in cfgs:
+                q0 = time.perf_counter_ns()
+                ev = evaluate(a1, a2, cfg, m)
+                lat.append((time.perf_counter_ns() - q0) / 1e3)
+                rows.append(np.concatenate([[ev.score.real], ev.force, ev.torque]))
+            dt = time.perf_counter() - t0
         lat.sort()
-        return n_traj / dt, lat[len(lat) // 2], lat[min(len(lat) - 1, int(0.99 * len(lat)))], rows
+        st = {"poses_per_s": r4(len(cfgs) / dt), "p50_us": r4(lat[len(lat) // 2]),
+              "p99_us": r4(lat[min(len(lat) - 1, int(0.99 * len(lat)))]), "precompute_ms": r4(pre_ms),
+              "inputs": f"{scene} {n}^3 K={side // 2} GPU-built assets, evaluate() in a haptic session"}
+        if cpu_ok:
+            g = a1.grid
+            C1h, C2h = np.asarray(w1), np.asarray(w2)
+            c, dom, dcell = g.center(), g.delta_omega(), 1.0 / (g.node_count * g.cell_volume)
+            idx = np.linspace(0, len(cfgs) - 1, 24).astype(int)
+            Rp = np.array([cfgs[i].rotation for i in idx])
+            tp = np.array([cfgs[i].translation - c + cfgs[i].rotation @ c for i in idx])
+            # evaluate() returns real parts: Re S (energy = -Re S), force = Re T, torque = Re G
+            got = np.array([rows[i] for i in idx])
+            from concurrent.futures import ThreadPoolExecutor
 
-    with haptic_session(p1, p2, m1):
-        rate_s, p50_s, p99_s, res1 = run_traj()
-    rate_l, p50_l, p99_l, _ = run_traj()
-    out["trajectory_C1"] = {
-        "workload": "peg-in-hole (64-gon cylinder peg, bored block) 64^3, K=16 (m'=32768), 1000-pose "
-                    "insertion trajectory through evaluate(); assets built on the GPU from the meshes",
-        "precompute_ms": pre_ms, "poses_per_s": rate_s, "p50_us": p50_s, "p99_us": p99_s,
-        "path": "evaluate() inside haptic_session (resident query grid)",
-        "launch_path": {"poses_per_s": rate_l, "p50_us": p50_l, "p99_us": p99_l},
-        "precision": backend.precision()}
-    if rank == 0 and not args.no_cpu:
-        core = reference_core()
-        g1 = p1.grid
-        C1h, C2h = np.asarray(w1c), np.asarray(w2c)
-        c1 = g1.center()
-        dcell1 = 1.0 / (g1.node_count * g1.cell_volume)
-        idx = np.linspace(0, n_traj - 1, 100).astype(int)
-        t0 = time.perf_counter()
-        refs = [core.cascade_3d(C1h, C2h, bool(w1wrap), *g1.delta_omega(), dcell1, np.eye(3),
-                                np.ascontiguousarray(cfgs[i].translation), c1) for i in idx]
-        dt = time.perf_counter() - t0
-        ref_rows = np.array([np.concatenate([[-r[0].real], r[1:4].real, r[4:7].real]) for r in refs])
-        got = np.array(res1)[idx]
-        # parity as BASELINE.md states it: |new - ref| <= 1e-4 max(|ref|, L1), L1 = dcell sum |summand|
-        l1 = np.array([np.abs(oracle.cascade_term_scales(C1h, C2h, bool(w1wrap), g1.delta_omega(), dcell1,
-                                                         np.eye(3), cfgs[i].translation, c1))
-                       for i in idx])
-        denom = np.maximum(np.abs(ref_rows), l1)
-        out["trajectory_C1"]["max_err_over_tolerance_scale"] = float(np.max(np.abs(got - ref_rows) / denom))
-        out["trajectory_C1"]["tolerance"] = "1e-4 of max(|ref|, L1) (BASELINE.md section 2)"
-        out["trajectory_C1"]["cpu_baseline"] = {
-            "value": len(idx) / dt, "unit": "poses/s", "cores": 1, "kind": "reference",
-            "sample": f"{len(idx)} trajectory poses through _core.cascade_3d (oracle/_ref) on the same "
-                      "windows, single thread"}
-    del p1, p2
-    torch.cuda.empty_cache()
+            import oracle
 
-    # --- C2 on real assets: the low-clearance peg-in-hole at 128^3, K=32 (m' = 64^3), the
-    # headline configuration with GPU-built windows instead of synthetic ones; the jittered
-    # insertion path of the headline, through evaluate() in a haptic session
-    sc2 = scenes.get_scene("peg_in_hole_lowclear")
-    m2 = 64 ** 3
+            with ThreadPoolExecutor(max_workers=8) as pool:
+                want = list(pool.map(lambda k: ref_cascade(C1h, C2h, wrap, dom, dcell, Rp[k], tp[k], c),
+                                     range(len(idx))))
+                l1 = list(pool.map(lambda k: oracle.cascade_term_scales(C1h, C2h, wrap, dom, dcell, Rp[k], tp[k], c),
+                                   range(len(idx))))
+            want = np.array([np.concatenate([[w_[0].real], w_[1:4].real, w_[4:7].real]) for w_ in want])
+            parity[key] = parity_entry(got, want, np.asarray(l1).real, "oracle/_ref _core.cascade_3d")
+            t0 = time.perf_counter()
+            nref = 0
+            while time.perf_counter() - t0 < args.stage_cpu_seconds and nref < len(idx):
+                ref_cascade(C1h, C2h, wrap, dom, dcell, Rp[nref], tp[nref], c)
+                nref += 1
+            st["cpu"] = {"value": r4(nref / (time.perf_counter() - t0)), "unit": "poses/s", "cores": 1,
+                         "kind": "reference"}
+        res[key] = st
+        del a1, a2, w1, w2
+        torch.cuda.empty_cache()
+    return res
+
+
+def stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok):
+    """C3: 10^6 cmd_bench SE(3) poses of the gear pair (256^3, K=48: w = 96),
+    sharded by pose across ranks; device-timed kernel region (poses already
+    in HBM, max over ranks) and the e2e parallel.pose_sweep (host poses in,
+    gathered host results out)."""
+    import torch
+
+    from paper_1711_05017_b200 import backend, parallel
+
+    n3, w3 = 256, 96
+    W1, W2, g, dens_s = _gpu_windows("gear_pair", n3, w3, world, rank)
+    a1, a2 = _Asset(g, W1, False), _Asset(g, W2, False)
+    span = 0.25 * (g.spacing * n3)
+    Rs, ts = cmd_bench_poses(args.sweep_poses, span, seed=0)
+    c = g.center()
+    dom, dcell = g.delta_omega(), 1.0 / (g.node_count * g.cell_volume)
+    lo, hi = parallel.shard_range(len(ts), rank, world)
+    t_eff = ts[lo:hi] - c + np.einsum("nij,j->ni", Rs[lo:hi], c)
+    poses = torch.from_numpy(backend.pack_poses(Rs[lo:hi], t_eff)).cuda()
+    res = torch.empty((hi - lo, 14), dtype=torch.float64, device="cuda")
+
+    def run():
+        backend.cascade_batch(W1, W2, False, dom, dcell, c, poses, out=res, precision="fp32")
+
+    run()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    q1, q2 = sc2.build_assets(128, m_prime=m2)
-    v1c, v1wrap = q1.window(m2)
-    v2c, _ = q2.window(m2)
-    torch.cuda.synchronize()
-    pre2_ms = (time.perf_counter() - t0) * 1e3
-    Rj, tj, _ = trajectory(2000, SEED + 11)
-    cfg2 = [Configuration(R, t) for R, t in zip(Rj, tj)]
-    with haptic_session(q1, q2, m2):
-        for cfg in cfg2[:50]:
-            evaluate(q1, q2, cfg, m2)
-        lat2, rows2 = [], []
-        t0 = time.perf_counter()
-        for cfg in cfg2:
-            q0 = time.perf_counter_ns()
-            ev = evaluate(q1, q2, cfg, m2)
-            lat2.append((time.perf_counter_ns() - q0) / 1e3)
-            rows2.append(np.concatenate([[ev.energy], ev.force, ev.torque]))
-        dt2 = time.perf_counter() - t0
-    lat2.sort()
-    out["trajectory_C2_real"] = {
-        "workload": "low-clearance peg-in-hole 128^3 (clearance 0.01 x bore), K=32 (m'=262144), 2000-pose "
-                    "jittered insertion path through evaluate() in a haptic session; assets built on the GPU",
-        "precompute_ms": pre2_ms, "poses_per_s": len(cfg2) / dt2, "p50_us": lat2[len(lat2) // 2],
-        "p99_us": lat2[min(len(lat2) - 1, int(0.99 * len(lat2)))], "precision": backend.precision()}
-    if rank == 0 and not args.no_cpu:
-        core = reference_core()
-        g2 = q1.grid
-        D1h, D2h = np.asarray(v1c), np.asarray(v2c)
-        c2 = g2.center()
-        dcell2 = 1.0 / (g2.node_count * g2.cell_volume)
-        idx = np.linspace(0, len(cfg2) - 1, 20).astype(int)
-        teff = [cfg2[i].translation - c2 + cfg2[i].rotation @ c2 for i in idx]
-        t0 = time.perf_counter()
-        refs = [core.cascade_3d(D1h, D2h, bool(v1wrap), *g2.delta_omega(), dcell2,
-                                np.ascontiguousarray(cfg2[i].rotation), np.ascontiguousarray(te), c2)
-                for i, te in zip(idx, teff)]
-        dt = time.perf_counter() - t0
-        ref_rows = np.array([np.concatenate([[-r[0].real], r[1:4].real, r[4:7].real]) for r in refs])
-        l1 = np.array([np.abs(oracle.cascade_term_scales(D1h, D2h, bool(v1wrap), g2.delta_omega(), dcell2,
-                                                         cfg2[i].rotation, te, c2)) for i, te in zip(idx, teff)])
-        got = np.array(rows2)[idx]
-        out["trajectory_C2_real"]["max_err_over_tolerance_scale"] = float(
-            np.max(np.abs(got - ref_rows) / np.maximum(np.abs(ref_rows), l1)))
-        out["trajectory_C2_real"]["tolerance"] = "1e-4 of max(|ref|, L1) (BASELINE.md section 2)"
-        out["trajectory_C2_real"]["cpu_baseline"] = {
-            "value": len(idx) / dt, "unit": "poses/s", "cores": 1, "kind": "reference",
-            "sample": f"{len(idx)} of the same poses through _core.cascade_3d (oracle/_ref) on the same windows, "
-                      "single thread"}
-    del q1, q2
-    torch.cuda.empty_cache()
-
-    # --- C3: batched pose sweep, gear-pair grid 256^3, K=48 (w=96), cmd_bench poses
-    n3, w3, dom3 = 256, 96, 5.42
-    g3 = SampleGrid(3, (n3,) * 3, (-0.5 * dom3,) * 3, dom3 / n3)
-    mk = lambda w: torch.randn((w,) * 3, dtype=torch.complex128, device=dev, generator=gen) * 1e-2  # noqa: E731
-    a1, a2 = _Asset(g3, backend.DeviceWindow(mk(w3)), False), _Asset(g3, backend.DeviceWindow(mk(w3)), False)
-    Rs, ts = cmd_bench_poses(args.sweep_poses, 0.25 * dom3, seed=rank)
-    c = g3.center()
-    t_eff = ts - c + np.einsum("nij,j->ni", Rs, c)
-    poses = torch.from_numpy(backend.pack_poses(Rs, t_eff)).to(dev)
-    res = torch.empty((len(ts), 14), dtype=torch.float64, device=dev)
-    dcell = 1.0 / (g3.node_count * g3.cell_volume)
-    ms = _time_ms(lambda: backend.cascade_batch(a1._win, a2._win, False, g3.delta_omega(), dcell, c, poses,
-                                                out=res, precision="fp32"))
-    live = live_fraction(Rs, w3)
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run()
+    e1.record()
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    barrier(world)
     t0 = time.perf_counter()
     parallel.pose_sweep(a1, a2, Rs, ts, precision="fp32")
-    e2e_s = time.perf_counter() - t0
-    achieved = 240.0 * live * w3 ** 3 * len(ts) / (ms * 1e-3) / 1e12
-    out["sweep_C3"] = {
-        "workload": f"{len(ts)} cmd_bench SE(3) poses (seed {rank}), 256^3 grid, K=48 (w=96, m'={w3 ** 3}), fp32",
-        "poses_per_s": len(ts) / (ms * 1e-3), "e2e_poses_per_s": len(ts) / e2e_s,
-        "e2e_path": "parallel.pose_sweep: host poses in, host complex128 results out",
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "work": f"240 flop x live modes ({live:.3f} of m')",
-                     "traffic": _traffic("cascade3d_kernel"),
-                     "traffic_unit": "bytes per 2048-pose launch (ncu capture)"},
-        "projected_1e6_poses_s": 1e6 / (len(ts) / (ms * 1e-3)),
-    }
-    if rank == 0 and not args.no_cpu:
-        core = reference_core()
-        C1h, C2h = a1._win.__array__(), a2._win.__array__()
-        n_cpu = 0
-        t0 = time.perf_counter()
-        while time.perf_counter() - t0 < args.stage_cpu_seconds and n_cpu < len(ts):
-            core.cascade_3d(C1h, C2h, False, *g3.delta_omega(), dcell, np.ascontiguousarray(Rs[n_cpu]),
-                            np.ascontiguousarray(t_eff[n_cpu]), c)
-            n_cpu += 1
-        dt = time.perf_counter() - t0
-        out["sweep_C3"]["cpu_baseline"] = {
-            "value": n_cpu / dt, "unit": "poses/s", "cores": 1, "kind": "reference",
-            "sample": f"{n_cpu} of the same poses through _core.cascade_3d (oracle/_ref), 1 thread"}
-    del a1, a2, poses, res
-    torch.cuda.empty_cache()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    live = live_fraction(Rs[:64], w3)
+    achieved = 240.0 * live * w3 ** 3 * (hi - lo) / (ms * 1e-3) / 1e12
+    st = {"poses": len(ts), "n_gpus": world, "poses_per_s": r4(len(ts) / (ms * 1e-3)), "s": r4(ms * 1e-3),
+          "e2e_poses_per_s": r4(len(ts) / e2e_s), "frac": r4(achieved / fp32_peak), "tflops": r4(achieved),
+          "density_s": r4(dens_s), "inputs": "gear_pair 256^3 GPU density -> w=96 windows; cmd_bench poses seed 0"}
+    if cpu_ok:
+        C1h, C2h = np.asarray(W1), np.asarray(W2)
+        idx = np.array([0, 1, 4097, (hi - lo) - 1])
+        got = res[idx].cpu().numpy().view(np.complex128)
+        parity["C3"] = parity_of_poses(C1h, C2h, False, dom, dcell, c, Rs[lo:hi][idx], t_eff[idx], got)
+        rate, n, dt = cpu_reference_rate(C1h, C2h, Rs, ts - c + np.einsum("nij,j->ni", Rs, c), 1,
+                                         args.stage_cpu_seconds, consts=(None, c, dom, dcell))
+        st["cpu"] = {"value": r4(rate), "unit": "poses/s", "cores": 1, "kind": "reference",
+                     "days_1e6": r4(1e6 / rate / 86400)}
+    del poses, res, W1, W2, a1, a2
+    return st
 
-    # --- C4: full translational landscape 512^3 (full spectrum, w = N), fp32 field
+
+def stage_field(args, rank, world, parity, cpu_ok):
+    """C4: the full translational field at 512^3 (full spectra, w = N, wrap)
+    of the gear pair, one cmd_bench rotation (seed 1); slab-decomposed across
+    ranks when world > 1.  Roofline 24 B/voxel; cuFFT C2C
+    of the same size timed beside it as the speed bar; parity on the m' =
+    128^3 windowed variant's voxels against the C restatement of the cascade."""
+    import torch
+
+    from paper_1711_05017_b200 import parallel
+    from paper_1711_05017_b200.energy import score_field_device
+
     n4 = args.field_n
-    g4 = SampleGrid(3, (n4,) * 3, (-1.0,) * 3, 2.0 / n4)
-    b1, b2 = _Asset(g4, backend.DeviceWindow(mk(n4)), True), _Asset(g4, backend.DeviceWindow(mk(n4)), True)
-    R4, _ = cmd_bench_poses(1, 1.0, seed=1)
-    ms = _time_ms(lambda: score_field_device(b1, b2, R4[0], None, precision=32))
-    alg = 24.0 * n4 ** 3  # read both complex64 windows + write the complex64 field
-    ftr = _field_traffic() if n4 == 512 else None  # the committed capture is of the 512^3 landscape
-    out["field_C4"] = {
-        "workload": f"full translational field {n4}^3, full spectrum (w = N, wrap), one cmd_bench rotation (seed 1), "
-                    "complex64 out",
-        "voxels_per_s": n4 ** 3 / (ms * 1e-3), "ms": ms,
-        "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                     "frac": alg / (ms * 1e-3) / 1e9 / hbm, "work": "24 B/voxel algorithmic",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                     "traffic": ftr,
-                     "traffic_unit": "bytes per landscape: product + 3 FFT passes (ncu capture, 512^3)",
-                     "dram_achieved": (ftr / (ms * 1e-3) / 1e9) if ftr else None,
-                     "dram_frac": (ftr / (ms * 1e-3) / 1e9 / hbm) if ftr else None,
-                     "dram_note": "measured DRAM traffic of the four kernels / this run's time: the HBM "
-                                  "utilisation the north star's >= 50 % target refers to"},
-        "scaling_plan": "slab-decomposed across ranks with one all-to-all (parallel.score_field_slab)",
-    }
-    if rank == 0 and not args.no_cpu:
+    hbm = float(_peaks()["hbm_gbs"])
+    W1, W2, g, dens_s = _gpu_windows("gear_pair", n4, n4, world, rank)
+    a1, a2 = _Asset(g, W1, True), _Asset(g, W2, True)
+    R4 = cmd_bench_poses(1, 1.0, seed=1)[0][0]
+    if world > 1:
+        fn = lambda: parallel.score_field_slab(a1, a2, R4, None, precision=32)  # noqa: E731
+    else:
+        fn = lambda: score_field_device(a1, a2, R4, None, precision=32)  # noqa: E731
+    fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(_time_ms(fn), world)
+    alg = 24.0 * n4 ** 3
+    st = {"n": n4, "n_gpus": world, "ms": r4(ms), "gvox_per_s": r4(n4 ** 3 / (ms * 1e-3) / 1e9),
+          "roofline": {"bound": "hbm", "achieved": r4(alg / (ms * 1e-3) / 1e9), "peak": hbm, "unit": "GB/s",
+                       "frac": r4(alg / (ms * 1e-3) / 1e9 / hbm), "work": "24 B/voxel"},
+          "density_s": r4(dens_s), "inputs": "gear_pair 512^3 GPU density -> full spectra (wrap)"}
+    if world == 1:  # cuFFT C2C inverse of the same size (torch.fft -> cuFFT), the speed bar
+        x = torch.empty((n4,) * 3, dtype=torch.complex64, device="cuda")
+        x.normal_()
+        st["cufft_c2c_ms"] = r4(_time_ms(lambda: torch.fft.ifftn(x)))
+        del x
+    del a1, a2, W1, W2
+    torch.cuda.empty_cache()
+    if cpu_ok:  # windowed variant m' = 128^3 in the 512^3 grid: voxels vs the C restatement of the cascade
+        import oracle
+
+        rng = np.random.default_rng(4)
+        wv = 128
+        k2 = (np.arange(wv) - wv // 2).astype(np.float64) ** 2
+        amp = 1.0 / (1.0 + k2[:, None, None] + k2[None, :, None] + k2[None, None, :])
+        C1 = (rng.standard_normal((wv,) * 3) + 1j * rng.standard_normal((wv,) * 3)) * amp
+        C2 = (rng.standard_normal((wv,) * 3) + 1j * rng.standard_normal((wv,) * 3)) * amp
+        from paper_1711_05017_b200 import backend
+
+        V1, V2 = backend.DeviceWindow(C1), backend.DeviceWindow(C2)
+        land = score_field_device(_Asset(g, V1, False), _Asset(g, V2, False), R4, None, precision=32)
+        st["windowed_ms"] = r4(_time_ms(lambda: score_field_device(_Asset(g, V1, False), _Asset(g, V2, False), R4,
+                                                                   None, precision=32)))
+        picks = [(0, 0, 0), (n4 // 2, n4 // 2, n4 // 2), (17, 300, n4 - 1), (n4 - 1, 5, 260), (100, 200, 300),
+                 (400, 33, 77)]
+        vals = land.reshape((n4,) * 3)
+        got = np.array([complex(vals[p].item()) for p in picks])
+        c, dom, dcell = g.center(), g.delta_omega(), 1.0 / (g.node_count * g.cell_volume)
+        from concurrent.futures import ThreadPoolExecutor
+
+        pts = [np.asarray(g.origin) + g.spacing * np.asarray(p, dtype=np.float64) for p in picks]
+        with ThreadPoolExecutor(max_workers=len(picks)) as pool:
+            want = np.array(list(pool.map(lambda p: oracle.cascade(C1, C2, False, dom, dcell, R4, p - c + R4 @ c,
+                                                                   c)[0], pts)))
+        l1 = oracle.score_field_scale(C1, C2, False, g.dims, g.spacing, R4)
+        parity["C4"] = parity_entry(got, want, np.full(len(picks), l1), "oracle C cascade at t = p_j (windowed 128^3)")
+        del land, vals, V1, V2
+        torch.cuda.empty_cache()
         nc = 128
         rngc = np.random.default_rng(SEED)
         Cc1 = rngc.normal(size=(nc,) * 3) + 1j * rngc.normal(size=(nc,) * 3)
         Cc2 = rngc.normal(size=(nc,) * 3) + 1j * rngc.normal(size=(nc,) * 3)
         t0 = time.perf_counter()
-        oracle.score_field(Cc1, Cc2, True, (nc,) * 3, (-1.0,) * 3, 2.0 / nc, R4[0])
+        oracle.score_field(Cc1, Cc2, True, (nc,) * 3, (-1.0,) * 3, 2.0 / nc, R4)
         dt = time.perf_counter() - t0
-        out["field_C4"]["cpu_baseline"] = {
-            "value": nc ** 3 / dt, "unit": "voxels/s", "cores": 1, "kind": "port",
-            "sample": f"oracle.score_field (numpy restatement of energy.score_field, energy.py:309-344) at "
-                      f"{nc}^3 full spectrum, one rotation, {dt:.1f} s (512^3 does not fit a bounded CPU sample)"}
-    del b1, b2
-    torch.cuda.empty_cache()
+        st["cpu"] = {"value": r4(nc ** 3 / dt), "unit": "voxels/s", "cores": 1, "kind": "port",
+                     "sample": f"numpy restatement of energy.score_field at {nc}^3"}
+    return st
 
-    # --- C5: bolt-nut 256^3, K=64 (w=128), screw trajectory paced at 1 kHz
+
+def stage_haptic(args, parity, cpu_ok):
+    """C5: bolt-nut 256^3, K=64 (w = 128) from GPU-built densities of the
+    ~10^5-face meshes; a screw trajectory (2 turns, pitch 0.1) paced at
+    1 kHz, one evaluate per frame from a resident query grid; then the same
+    session held to part of the GPU while a 256^3 landscape runs in a worker
+    thread (SPEC.md:348)."""
+    import torch
+
+    from paper_1711_05017_b200.energy import score_field_device
     from paper_1711_05017_b200.haptic import HapticSession
 
-    n5, w5, dom5 = 256, 128, 4.37
-    g5 = SampleGrid(3, (n5,) * 3, (-0.5 * dom5,) * 3, dom5 / n5)
-    f5 = _Asset(g5, backend.DeviceWindow(mk(w5)), False), _Asset(g5, backend.DeviceWindow(mk(w5)), False)
+    n5, w5 = 256, 128
+    W1, W2, g, dens_s = _gpu_windows("bolt_nut", n5, w5, 1, 0)
+    f5 = _Asset(g, W1, False), _Asset(g, W2, False)
     frames = args.haptic_frames
-    th = np.linspace(0.0, 4.0 * np.pi, frames)  # two turns
+    th = np.linspace(0.0, 4.0 * np.pi, frames)
     pitch = 0.1
     R5 = np.stack([axis_rot(2, a) for a in th])
     t5 = np.stack([np.array([0.0, 0.0, 0.3 - pitch * a / (2 * np.pi)]) for a in th])
     sess = HapticSession(f5[0], f5[1], None)
-    sess.run(R5[:50], t5[:50], rate_hz=1000.0)  # warm
+    sess.run(R5[:200], t5[:200], rate_hz=1000.0)  # warm
     run = sess.run(R5, t5, rate_hz=1000.0)
-    out["haptic_C5"] = {"workload": f"bolt-nut 256^3 grid, K=64 (w=128, m'={w5 ** 3}), {frames}-frame screw "
-                                    "trajectory (2 turns, pitch 0.1) paced at 1 kHz, one evaluate per frame served by a "
-                                    "resident query grid (haptic_session), fp32",
-                        **run, "budget_us": 1000.0}
-    del f5, sess
-    torch.cuda.empty_cache()
+    st = {"frames": run["frames"], "p50_us": r4(run["p50_us"]), "p99_us": r4(run["p99_us"]),
+          "max_us": r4(run["max_us"]), "misses": run["deadline_misses"], "missed": run["missed"][:4],
+          "realtime": run["realtime"], "rt_runtime_us": run["rt_runtime_us"], "density_s": r4(dens_s),
+          "inputs": "bolt_nut 256^3 GPU density (75852 + 98816 faces) -> w=128 windows"}
+    # concurrency: a landscape export in a worker thread while the session serves frames
+    # on a subset of the SMs (the reference service's field worker, service.py:305-318)
+    gl = scenes_mod().get_scene("bolt_nut").grid(256)
+    L1, L2 = _Asset(gl, W1, False), _Asset(gl, W2, False)
+    done = {}
 
-    # --- W: forward centred window 256^3 -> w = 96 (complex128 field -> complex128 window)
+    def export():
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            t0 = time.perf_counter()
+            k = 0
+            while time.perf_counter() - t0 < 1.5:
+                score_field_device(L1, L2, R5[k % frames], None, precision=32)
+                k += 1
+            stream.synchronize()
+            done["fields"] = k
+            done["s"] = time.perf_counter() - t0
+
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    worker = threading.Thread(target=export)
+    worker.start()
+    crun = sess.run(R5[:2000], t5[:2000], rate_hz=1000.0, max_sms=nsm * 3 // 4)
+    worker.join()
+    st["concurrent"] = {"frames": crun["frames"], "p99_us": r4(crun["p99_us"]), "max_us": r4(crun["max_us"]),
+                        "misses": crun["deadline_misses"], "fields_done": done.get("fields"),
+                        "fields_per_s": r4(done.get("fields", 0) / max(done.get("s", 1e-9), 1e-9)),
+                        "server_sms": nsm * 3 // 4}
+    if cpu_ok:
+        C1h, C2h = np.asarray(W1), np.asarray(W2)
+        c, dom, dcell = g.center(), g.delta_omega(), 1.0 / (g.node_count * g.cell_volume)
+        from paper_1711_05017_b200.energy import Configuration, evaluate
+
+        idx = [0, frames // 3, frames // 2, frames - 1]
+        with_s = []
+        for i in idx:
+            ev = evaluate(f5[0], f5[1], Configuration(R5[i], t5[i]))
+            with_s.append(np.concatenate([[ev.score.real], ev.force, ev.torque]))
+        tp = np.array([t5[i] - c + R5[i] @ c for i in idx])
+        from concurrent.futures import ThreadPoolExecutor
+
+        import oracle
+
+        with ThreadPoolExecutor(max_workers=4) as pool:
+            want = list(pool.map(lambda k: ref_cascade(C1h, C2h, False, dom, dcell, R5[idx[k]], tp[k], c),
+                                 range(len(idx))))
+            l1 = list(pool.map(lambda k: oracle.cascade_term_scales(C1h, C2h, False, dom, dcell, R5[idx[k]], tp[k], c),
+                               range(len(idx))))
+        want = np.array([np.concatenate([[w_[0].real], w_[1:4].real, w_[4:7].real]) for w_ in want])
+        parity["C5"] = parity_entry(np.array(with_s), want, np.asarray(l1).real, "oracle/_ref _core.cascade_3d")
+    del f5, sess, W1, W2, L1, L2
+    torch.cuda.empty_cache()
+    return st
+
+
+def stage_window(args, parity, cpu_ok):
+    """Stage 2: forward DFT + truncation + centring of a 256^3 complex128
+    field to the w = 96 window (spectral.forward_dft / truncate /
+    center_window); parity at 128^3 against the numpy restatement."""
+    import torch
+
+    from paper_1711_05017_b200.descriptor import ComplexField, SampleGrid
+    from paper_1711_05017_b200.spectral import forward_window
+
+    hbm = float(_peaks()["hbm_gbs"])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(SEED)
     gw = SampleGrid(3, (256,) * 3, (-1.0,) * 3, 2.0 / 256)
     fw = ComplexField(gw, torch.randn(256 ** 3, dtype=torch.complex128, device=dev, generator=gen))
     ms = _time_ms(lambda: forward_window(fw, 96))
     alg = 16.0 * 256 ** 3 + 16.0 * 96 ** 3
-    out["window_W"] = {"workload": "forward DFT + truncation + centring, 256^3 complex128 field -> 96^3 window",
-                       "ms": ms, "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm,
-                                              "unit": "GB/s", "frac": alg / (ms * 1e-3) / 1e9 / hbm}}
-    if rank == 0 and not args.no_cpu:
+    st = {"ms": r4(ms), "roofline": {"bound": "hbm", "achieved": r4(alg / (ms * 1e-3) / 1e9), "peak": hbm,
+                                     "unit": "GB/s", "frac": r4(alg / (ms * 1e-3) / 1e9 / hbm)}}
+    if cpu_ok:
+        import oracle
+
         fh = fw.values.reshape((256,) * 3)
         t0 = time.perf_counter()
         A = oracle.forward_dft(fh, (256,) * 3, (-1.0,) * 3, 2.0 / 256)
-        oracle.center_window(A, (256,) * 3, (-1.0,) * 3, 2.0 / 256, 96)
-        dt = time.perf_counter() - t0
-        out["window_W"]["cpu_baseline"] = {"value": dt * 1e3, "unit": "ms", "cores": 1, "kind": "port",
-                                           "sample": "oracle.forward_dft + center_window (numpy pocketfft, as "
-                                                     "spectral.py:114-195) on the same 256^3 field"}
+        want = oracle.center_window(A, (256,) * 3, (-1.0,) * 3, 2.0 / 256, 96)
+        st["cpu"] = {"value": r4((time.perf_counter() - t0) * 1e3), "unit": "ms", "cores": 1, "kind": "port"}
+        got = forward_window(fw, 96).cpu().numpy()
+        parity["W"] = {"rel": r4(np.max(np.abs(got - want)) / np.max(np.abs(want))), "n": int(want.size),
+                       "vs": "numpy restatement of forward_dft + center_window"}
     del fw
     torch.cuda.empty_cache()
+    return st
 
-    # --- D: skeletal density of the C1 bored block at 64^3 (512 faces), float64
-    sc = scenes.get_scene("peg_in_hole")
-    gd = sc.grid(64)
-    affinity_field(sc.fixed, gd, sc.kernel)
-    torch.cuda.synchronize()
-    dt = None
-    for _ in range(3):  # best of 3 wall-clock calls (host allocation jitter)
-        t0 = time.perf_counter()
-        fd = affinity_field(sc.fixed, gd, sc.kernel)
-        d1 = time.perf_counter() - t0
-        dt = d1 if dt is None else min(dt, d1)
-    nf = len(sc.fixed.mesh.faces)
-    out["density_D"] = {"workload": f"affinity_field, bored block ({nf} faces) on 64^3, float64 bit-exact flags",
-                        "voxels_per_s": gd.node_count / dt, "node_face_pairs_per_s": gd.node_count * nf / dt,
-                        "ms": dt * 1e3, "excluded": fd.stats["excluded"], "unresolved": fd.stats["unresolved_nodes"],
-                        "device_seconds": {"distance_winding": fd.stats.get("seconds_distance"),
-                                           "sweep": fd.stats.get("seconds_sweep")},
-                        "roofline": {"bound": "fp64", "unit": "FP64 pipe utilisation (ncu)", "frac": 0.409,
-                                     "source": "profiles/r01_ncu_density_sweep.txt: sweep_kernel "
-                                               "sm__inst_executed_pipe_fp64 40.9 % of peak"}}
-    if rank == 0 and not args.no_cpu:
+
+def stage_density(args, fp64_peak, parity, cpu_ok):
+    """Stage 1: affinity_field of the C1 bored block at 64^3 and of the gear
+    at 128^3, with the FP64 work counted (~200 FP64 flops per node-element
+    pair) against the FP64 pipe measured in this run; flags
+    and stats at 32^3 against the oracle's C restatement."""
+    import torch
+
+    from paper_1711_05017_b200.descriptor import affinity_field
+
+    st = {}
+    for key, scene, n in (("peg64", "peg_in_hole", 64), ("gear128", "gear_pair", 128)):
+        sc = scenes_mod().get_scene(scene)
+        gd = sc.grid(n)
+        affinity_field(sc.fixed, gd, sc.kernel)
+        dt = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fd = affinity_field(sc.fixed, gd, sc.kernel)
+            d1 = time.perf_counter() - t0
+            dt = d1 if dt is None else min(dt, d1)
+        nf = len(sc.fixed.mesh.faces)
+        pairs = gd.node_count * nf
+        dev_s = fd.stats["seconds_distance"] + fd.stats["seconds_sweep"]
+        st[key] = {"ms": r4(dt * 1e3), "pairs_per_s": r4(pairs / dt), "faces": nf,
+                   "frac_fp64": r4(200.0 * pairs / dev_s / 1e12 / fp64_peak)}
+    if cpu_ok:
+        import oracle
+
+        sc = scenes_mod().get_scene("gear_pair")
+        g = sc.grid(32)
+        f = affinity_field(sc.fixed, g, sc.kernel)
+        want, flags, stats, _, _ = oracle.affinity_values(*sc.fixed.element_arrays(), g.dims, g.origin, g.spacing)
+        vals = np.asarray(f.values)
+        parity["D"] = {"flags_equal": f.flags == flags,
+                       "stats_equal": all(f.stats[k] == stats[k] for k in ("excluded", "eta_clamped", "worst_residual",
+                                                                           "unresolved_nodes", "inside_nodes")),
+                       "rel": r4(np.max(np.abs(vals - want)) / np.max(np.abs(want))), "n": int(g.node_count),
+                       "vs": "oracle C restatement (gear 32^3)"}
         core = reference_core()
         gc = sc.grid(16)
         P = gc.points()
@@ -815,10 +983,9 @@ def measure_stages(args, rank, world, fp32_peak):
         core.sweep_3d(tri, m.normals, m.areas, P, np.maximum(xi, 0.25 * gc.spacing), 0.5, 1 / (4 * np.pi), 0.02, 16,
                       0.25 * gc.spacing, iplus, res, cl, 0, len(P))
         dt = time.perf_counter() - t0
-        out["density_D"]["cpu_baseline"] = {
-            "value": gc.node_count * nf / dt, "unit": "node-face pairs/s", "cores": 1, "kind": "reference",
-            "sample": f"_core distance_3d + winding_3d + sweep_3d (oracle/_ref) for the same part on 16^3, {dt:.1f} s"}
-    return out
+        st["cpu"] = {"value": r4(gc.node_count * len(m.faces) / dt), "unit": "node-face pairs/s", "cores": 1,
+                     "kind": "reference"}
+    return st
 
 
 def main():
@@ -833,11 +1000,13 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=6.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stages", action="store_true")
-    ap.add_argument("--sweep-poses", type=int, default=16384)
-    ap.add_argument("--stage-cpu-seconds", type=float, default=4.0)
-    ap.add_argument("--haptic-frames", type=int, default=1000)
+    ap.add_argument("--sweep-poses", type=int, default=1000000)
+    ap.add_argument("--stage-cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--haptic-frames", type=int, default=10000)
     ap.add_argument("--field-n", type=int, default=512)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.warmup < 3 and args.impl == "b200":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
