@@ -263,8 +263,9 @@ def reference_core():
 
 def ref_cascade(C1, C2, wrap, dom, dcell, R, t_eff, c):
     core = reference_core()
-    return np.asarray(core.cascade_3d(np.ascontiguousarray(C1), np.ascontiguousarray(C2), bool(wrap), *dom, dcell,
-                                      np.ascontiguousarray(R), np.ascontiguousarray(t_eff), np.ascontiguousarray(c)))
+    wr = lambda x, dt=np.float64: np.require(x, dtype=dt, requirements=["C", "W"])  # noqa: E731  (memoryviews)
+    return np.asarray(core.cascade_3d(wr(C1, np.complex128), wr(C2, np.complex128), bool(wrap), *[float(v) for v in dom],
+                                      float(dcell), wr(R), wr(t_eff), wr(c)))
 
 
 def parity_entry(got, want, l1, against):

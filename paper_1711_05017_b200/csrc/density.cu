@@ -25,13 +25,18 @@
 
 #include <math.h>
 
+#include <algorithm>
+#include <cmath>
+#include <cstring>
 #include <map>
 #include <string.h>
+#include <vector>
 
 namespace gf {
 namespace {
 
 constexpr int kThreads = 128;
+constexpr int kSweepThreads = 256;
 constexpr int kTile = 128;  // elements per shared-memory tile
 
 struct d3 { double x, y, z; };
@@ -176,6 +181,97 @@ __global__ void __launch_bounds__(kThreads) dist_wind_kernel(PointSource src, co
 }
 
 // ---------------------------------------------------------------------------
+// D1a + D1b on grid nodes, culled (3D).  Same values and decisions as
+// dist_wind_kernel, with less work per node:
+//  * distance: the elements are also kept in a spatially sorted copy whose
+//    tiles carry a bounding sphere (centre, inflated radius).  A node's
+//    upper bound on its min distance is |p - c_t| + r_t of its nearest tile
+//    centre; a tile whose lower bound |p - c_t| - r_t exceeds that (with a
+//    1e-9 relative margin) cannot hold the minimum and is skipped.  The min
+//    is order-independent, so the value is the same bits as the full loop
+//    (the reference's BVH prunes the same way, _core.pyx:189-230).
+//  * winding: with `wind_bbox`, a node outside the (closed) mesh's inflated
+//    bounding box has winding number 0 up to rounding, so `inside` is false
+//    exactly as in the reference; the sum is skipped and 0 stored.  Used
+//    only where the winding value itself is not returned (the skeletal
+//    family, where it decides occupancy alone).
+// Tiles are loaded only when some node of the block needs them.
+struct CullInfo {
+  const double* sorted;    // ne x 9, spatially ordered copy of the elements
+  const double4* spheres;  // per kTile tile of `sorted`: centre xyz, radius
+  int ntiles;
+  int wind_bbox;           // 1: winding only for nodes inside [lo, hi]
+  double lo[3], hi[3];
+};
+
+__global__ void __launch_bounds__(kThreads) dist_wind_culled_kernel(PointSource src, const double* __restrict__ elems,
+                                                                    int64_t ne, int64_t m, CullInfo ci,
+                                                                    double* __restrict__ xi_out,
+                                                                    double* __restrict__ wind_out) {
+  __shared__ double tile[kTile * 9];
+  const int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x;
+  const bool live = i < m;
+  double p[3] = {0.0, 0.0, 0.0};
+  if (live) src.get(i, p);
+  const d3 pp = {p[0], p[1], p[2]};
+  double best = 1e300;
+  if (xi_out) {
+    // upper bound of the min distance from the nearest tile centre
+    double dmin2 = 1e300, rsel = 0.0;
+    for (int t = 0; t < ci.ntiles; ++t) {
+      const double4 s = ci.spheres[t];
+      const double dx = p[0] - s.x, dy = p[1] - s.y, dz = p[2] - s.z;
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      if (d2 < dmin2) {
+        dmin2 = d2;
+        rsel = s.w;
+      }
+    }
+    const double lim = (sqrt(dmin2) + rsel) * (1.0 + 1e-9);
+    for (int t = 0; t < ci.ntiles; ++t) {
+      const double4 s = ci.spheres[t];
+      const double dx = p[0] - s.x, dy = p[1] - s.y, dz = p[2] - s.z;
+      const double reach = lim + s.w;
+      const bool need = live && dx * dx + dy * dy + dz * dz <= reach * reach;
+      if (!__syncthreads_or(need)) continue;
+      const int64_t e0 = (int64_t)t * kTile;
+      const int n = (int)min((int64_t)kTile, ne - e0);
+      for (int k = threadIdx.x; k < n * 9; k += kThreads) tile[k] = ci.sorted[e0 * 9 + k];
+      __syncthreads();
+      if (need) {
+        for (int e = 0; e < n; ++e) {
+          const double* q = tile + e * 9;
+          const double dd = tri_dist({q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}, pp);
+          if (dd < best) best = dd;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (wind_out) {
+    const bool inb = p[0] >= ci.lo[0] && p[0] <= ci.hi[0] && p[1] >= ci.lo[1] && p[1] <= ci.hi[1] &&
+                     p[2] >= ci.lo[2] && p[2] <= ci.hi[2];
+    const bool need = live && (!ci.wind_bbox || inb);
+    double acc = 0.0;
+    if (__syncthreads_or(need)) {
+      for (int64_t e0 = 0; e0 < ne; e0 += kTile) {  // original element order: the reference's summation order
+        const int n = (int)min((int64_t)kTile, ne - e0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < n * 9; k += kThreads) tile[k] = elems[e0 * 9 + k];
+        __syncthreads();
+        if (!need) continue;
+        for (int e = 0; e < n; ++e) {
+          const double* q = tile + e * 9;
+          acc += solid_angle({q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}, pp);
+        }
+      }
+    }
+    if (live) wind_out[i] = need ? acc / 12.566370614359172 : 0.0;
+  }
+  if (live && xi_out) xi_out[i] = best;
+}
+
+// ---------------------------------------------------------------------------
 // D1c: adaptive skeletal sweep
 
 struct SweepParams {
@@ -221,15 +317,24 @@ __device__ __forceinline__ Tri child_tri(const Tri& P, int k) {
   return Tri{P.a, m01, m02};
 }
 
+// kSweepThreads nodes per CTA share every staged element tile (the kernel is
+// bound by the L2 -> shared traffic of the tiles at ~10^5 elements).
+// 3D tiles also carry each triangle's bounding radius about its centroid
+// (`radii`, inflated): at depth 0, if area / (|p - centroid| - r)^2 is
+// below max_angle (1e-9 margin), the reference's measure test
+// area / (dist^2 + 1e-300) > max_angle cannot fire, so the exact distance is
+// not needed -- the face is a leaf, with the same bits and no residual.
 template <int D>
-__global__ void __launch_bounds__(kThreads) sweep_kernel(PointSource src, const double* __restrict__ elems,
-                                                         const double* __restrict__ normals,
-                                                         const double* __restrict__ measures, int64_t ne, int64_t m,
-                                                         const double* __restrict__ xi_eff, SweepParams sp,
-                                                         double* __restrict__ out, double* __restrict__ resid,
-                                                         int64_t* __restrict__ clamps) {
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, const double* __restrict__ elems,
+                                                              const double* __restrict__ normals,
+                                                              const double* __restrict__ measures,
+                                                              const double* __restrict__ radii, int64_t ne, int64_t m,
+                                                              const double* __restrict__ xi_eff, SweepParams sp,
+                                                              double* __restrict__ out, double* __restrict__ resid,
+                                                              int64_t* __restrict__ clamps) {
   constexpr int E = D == 3 ? 9 : 4;
-  constexpr int ET = E + D + 1;  // element + normal + measure
+  constexpr int ET = E + D + 1 + (D == 3 ? 1 : 0);  // element + normal + measure (+ radius)
+  constexpr int kThreads = kSweepThreads;
   __shared__ double tile[kTile * ET];
   const int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x;
   const bool live = i < m;
@@ -250,6 +355,8 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(PointSource src, const 
     for (int t = threadIdx.x; t < n * E; t += kThreads) tile[(t / E) * ET + t % E] = elems[e0 * E + t];
     for (int t = threadIdx.x; t < n * D; t += kThreads) tile[(t / D) * ET + E + t % D] = normals[e0 * D + t];
     for (int t = threadIdx.x; t < n; t += kThreads) tile[t * ET + E + D] = measures[e0 + t];
+    if (D == 3)
+      for (int t = threadIdx.x; t < n; t += kThreads) tile[t * ET + E + D + 1] = radii[e0 + t];
     __syncthreads();
     if (!live) continue;
     for (int e = 0; e < n; ++e) {
@@ -261,6 +368,16 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(PointSource src, const 
       Tri cur;
       if (D == 3) cur = Tri{{q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}};
       else cur = Tri{{q[0], q[1], 0.0}, {q[2], q[3], 0.0}, {0.0, 0.0, 0.0}};
+      if (D == 3) {  // far face: a depth-0 leaf without the exact distance (see above)
+        const double mx = (cur.a.x + cur.b.x + cur.c.x) / 3.0 - p.x;
+        const double my = (cur.a.y + cur.b.y + cur.c.y) / 3.0 - p.y;
+        const double mz = (cur.a.z + cur.b.z + cur.c.z) / 3.0 - p.z;
+        const double lb = sqrt(mx * mx + my * my + mz * mz) - q[E + D + 1];
+        if (lb > 0.0 && meas < sp.max_angle * (lb * lb) * (1.0 - 1e-9)) {
+          leaf_3d(cur.a, cur.b, cur.c, meas, p, nrm, xi, sp, re, im, ncl);
+          continue;
+        }
+      }
       while (true) {
         double measure;
         if (D == 3) {
@@ -495,6 +612,103 @@ int check_dim(int d) {
   return 0;
 }
 
+// Per-triangle bounding radius about the centroid (a + b + c) / 3, inflated
+// so rounding can only make it larger (the sweep's depth-0 shortcut).
+std::vector<double> triangle_radii(const double* el, int64_t ne) {
+  std::vector<double> r(ne);
+  for (int64_t e = 0; e < ne; ++e) {
+    const double* q = el + 9 * e;
+    const double c[3] = {(q[0] + q[3] + q[6]) / 3.0, (q[1] + q[4] + q[7]) / 3.0, (q[2] + q[5] + q[8]) / 3.0};
+    double m = 0.0;
+    for (int v = 0; v < 3; ++v) {
+      const double dx = q[3 * v] - c[0], dy = q[3 * v + 1] - c[1], dz = q[3 * v + 2] - c[2];
+      m = std::max(m, std::sqrt(dx * dx + dy * dy + dz * dz));
+    }
+    r[e] = m * (1.0 + 1e-12) + 1e-300;
+  }
+  return r;
+}
+
+// Culling aids of a closed triangle set for dist_wind_culled_kernel: the
+// elements in Morton order of their centroids (compact tiles), one inflated
+// bounding sphere per tile, and the inflated bounding box.
+struct CullHost {
+  std::vector<double> sorted;
+  std::vector<double4> spheres;
+  double lo[3], hi[3];
+};
+
+void build_cull(const double* el, int64_t ne, CullHost& h) {
+  for (int a = 0; a < 3; ++a) {
+    h.lo[a] = 1e300;
+    h.hi[a] = -1e300;
+  }
+  for (int64_t v = 0; v < 3 * ne; ++v)  // every vertex of every triangle
+    for (int a = 0; a < 3; ++a) {
+      h.lo[a] = std::min(h.lo[a], el[3 * v + a]);
+      h.hi[a] = std::max(h.hi[a], el[3 * v + a]);
+    }
+  double ext = 0.0;
+  for (int a = 0; a < 3; ++a) ext = std::max(ext, h.hi[a] - h.lo[a]);
+  std::vector<std::pair<uint32_t, int64_t>> key(ne);
+  for (int64_t e = 0; e < ne; ++e) {
+    const double* q = el + 9 * e;
+    uint32_t code = 0;
+    for (int a = 0; a < 3; ++a) {
+      const double c = (q[a] + q[3 + a] + q[6 + a]) / 3.0;
+      uint32_t v = (uint32_t)std::min(1023.0, std::max(0.0, (c - h.lo[a]) / (ext + 1e-300) * 1024.0));
+      for (int b = 0; b < 10; ++b) code |= ((v >> b) & 1u) << (3 * b + a);
+    }
+    key[e] = {code, e};
+  }
+  std::stable_sort(key.begin(), key.end());
+  h.sorted.resize(9 * ne);
+  for (int64_t e = 0; e < ne; ++e) std::memcpy(&h.sorted[9 * e], el + 9 * key[e].second, 9 * sizeof(double));
+  const int64_t nt = ceil_div(ne, kTile);
+  h.spheres.resize(nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    const int64_t e1 = std::min(ne, (t + 1) * kTile);
+    for (int64_t e = t * kTile; e < e1; ++e)
+      for (int v = 0; v < 3; ++v)
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = std::min(lo[a], h.sorted[9 * e + 3 * v + a]);
+          hi[a] = std::max(hi[a], h.sorted[9 * e + 3 * v + a]);
+        }
+    const double c[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+    double r = 0.0;
+    for (int64_t e = t * kTile; e < e1; ++e)
+      for (int v = 0; v < 3; ++v) {
+        const double* q = &h.sorted[9 * e + 3 * v];
+        const double dx = q[0] - c[0], dy = q[1] - c[1], dz = q[2] - c[2];
+        r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz));
+      }
+    h.spheres[t] = make_double4(c[0], c[1], c[2], r * (1.0 + 1e-12) + 1e-300);
+  }
+  for (int a = 0; a < 3; ++a) {
+    const double pad = 1e-9 * (ext + std::fabs(h.lo[a]) + std::fabs(h.hi[a]));
+    h.lo[a] -= pad;
+    h.hi[a] += pad;
+  }
+}
+
+// upload the culling aids; ci points into the device buffers
+int upload_cull(const CullHost& h, int64_t ne, int wind_bbox, DevBuf& ds, DevBuf& dsp, CullInfo& ci,
+                cudaStream_t st) {
+  int rc = upload(h.sorted.data(), sizeof(double) * 9 * ne, ds, st);
+  if (rc) return rc;
+  if ((rc = upload(h.spheres.data(), sizeof(double4) * h.spheres.size(), dsp, st))) return rc;
+  ci.sorted = (const double*)ds.p;
+  ci.spheres = (const double4*)dsp.p;
+  ci.ntiles = (int)h.spheres.size();
+  ci.wind_bbox = wind_bbox;
+  for (int a = 0; a < 3; ++a) {
+    ci.lo[a] = h.lo[a];
+    ci.hi[a] = h.hi[a];
+  }
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -538,7 +752,6 @@ int gf_winding_grid(int d, const double* elems, int64_t ne, const int32_t* dims,
   DevBuf de, dx;
   const int E = d == 3 ? 9 : 4;
   if ((rc = upload(elems, sizeof(double) * E * ne, de, st))) return rc;
-  GF_CUDA(dx.alloc(sizeof(double) * m));  // the kernel writes distances too
   PointSource src = {};
   src.P = nullptr;
   src.d = d;
@@ -548,9 +761,14 @@ int gf_winding_grid(int d, const double* elems, int64_t ne, const int32_t* dims,
   }
   src.spacing = spacing;
   unsigned grid = (unsigned)ceil_div(m, kThreads);
-  if (d == 3)
-    dist_wind_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dx.p, (double*)wind_dev);
-  else
+  if (d == 3) {  // winding only (the exact sum at every node: the indicator returns the value)
+    CullInfo ci = {};
+    dist_wind_culled_kernel<<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, ci, nullptr,
+                                                       (double*)wind_dev);
+  } else {
+    GF_CUDA(dx.alloc(sizeof(double) * m));  // the 2D kernel writes distances too
+  }
+  if (d == 2)
     dist_wind_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dx.p, (double*)wind_dev);
   GF_CUDA(cudaGetLastError());
   GF_CUDA(cudaStreamSynchronize(st));  // the element and distance buffers go back to the cache
@@ -581,15 +799,21 @@ int gf_sweep(int d, const double* elems, const double* normals, const double* me
   src.P = (const double*)dp.p;
   src.d = d;
   SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
-  unsigned grid = (unsigned)ceil_div(m, kThreads);
-  if (d == 3)
-    sweep_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p, (const double*)dm.p, ne,
-                                               m, (const double*)dx.p, sp, (double*)dout.p, (double*)dres.p,
-                                               (int64_t*)dcl.p);
-  else
-    sweep_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p, (const double*)dm.p, ne,
-                                               m, (const double*)dx.p, sp, (double*)dout.p, (double*)dres.p,
-                                               (int64_t*)dcl.p);
+  unsigned grid = (unsigned)ceil_div(m, kSweepThreads);
+  DevBuf drad;
+  std::vector<double> radii;
+  if (d == 3) {
+    radii = triangle_radii(elems, ne);
+    if ((rc = upload(radii.data(), sizeof(double) * ne, drad, st))) return rc;
+    sweep_kernel<3><<<grid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
+                                                    (const double*)dm.p, (const double*)drad.p, ne, m,
+                                                    (const double*)dx.p, sp, (double*)dout.p, (double*)dres.p,
+                                                    (int64_t*)dcl.p);
+  } else {
+    sweep_kernel<2><<<grid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
+                                                    (const double*)dm.p, nullptr, ne, m, (const double*)dx.p, sp,
+                                                    (double*)dout.p, (double*)dres.p, (int64_t*)dcl.p);
+  }
   GF_CUDA(cudaGetLastError());
   GF_CUDA(cudaMemcpyAsync(out_c128, dout.p, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, st));
   GF_CUDA(cudaMemcpyAsync(resid, dres.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
@@ -663,10 +887,22 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     }
   } ev_guard{ev};
   GF_CUDA(cudaEventRecord(ev[0], st));
-  if (d == 3)
-    dist_wind_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dxi.p, (double*)dwind.p);
-  else
+  DevBuf dsorted, dspheres, drad;
+  std::vector<double> radii;
+  if (d == 3) {
+    // winding values leave this pipeline only for the inverse-square family;
+    // the skeletal family needs occupancy alone (the bounding-box shortcut)
+    CullHost ch;
+    build_cull(elems, ne, ch);
+    CullInfo ci;
+    if ((rc = upload_cull(ch, ne, family != 0 ? 1 : 0, dsorted, dspheres, ci, st))) return rc;
+    dist_wind_culled_kernel<<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, ci, (double*)dxi.p,
+                                                       (double*)dwind.p);
+    radii = triangle_radii(elems, ne);
+    if ((rc = upload(radii.data(), sizeof(double) * ne, drad, st))) return rc;
+  } else {
     dist_wind_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dxi.p, (double*)dwind.p);
+  }
   GF_CUDA(cudaGetLastError());
   GF_CUDA(cudaEventRecord(ev[1], st));
   if (family != 0) {
@@ -675,14 +911,16 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     clamp_min_kernel<<<sm_count() * 8, 256, 0, st>>>((const double*)dxi.p, (double*)dxe.p, m, eta_min);
     GF_CUDA(cudaGetLastError());
     SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
+    const unsigned sgrid = (unsigned)ceil_div(m, kSweepThreads);
     if (d == 3)
-      sweep_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p, (const double*)dm.p,
-                                                 ne, m, (const double*)dxe.p, sp, (double*)dip.p, (double*)dres.p,
-                                                 (int64_t*)dcl.p);
+      sweep_kernel<3><<<sgrid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
+                                                       (const double*)dm.p, (const double*)drad.p, ne, m,
+                                                       (const double*)dxe.p, sp, (double*)dip.p, (double*)dres.p,
+                                                       (int64_t*)dcl.p);
     else
-      sweep_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p, (const double*)dm.p,
-                                                 ne, m, (const double*)dxe.p, sp, (double*)dip.p, (double*)dres.p,
-                                                 (int64_t*)dcl.p);
+      sweep_kernel<2><<<sgrid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
+                                                       (const double*)dm.p, nullptr, ne, m, (const double*)dxe.p, sp,
+                                                       (double*)dip.p, (double*)dres.p, (int64_t*)dcl.p);
     GF_CUDA(cudaGetLastError());
   }
   GF_CUDA(cudaEventRecord(ev[2], st));
