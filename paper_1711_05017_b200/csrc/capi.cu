@@ -552,7 +552,11 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   if (rc) return rc;
   a.partials = sc.partials;
   a.counters = sc.counters;
-  // one single-query launch per pose, stream-ordered (the haptic loop shape)
+  // one single-query launch per pose, stream-ordered (the haptic loop shape);
+  // programmatic dependent launch lets query i+1's pose setup and mode loop
+  // run under query i's reduction tail -- its shared-scratch stage still
+  // waits for query i to complete (griddepcontrol.wait)
+  a.pdl = 1;
   cudaError_t le = cudaSuccess;
   for (int64_t i = 0; i < n && le == cudaSuccess; ++i) {
     a.poses = poses_dev + 12 * i;

@@ -31,6 +31,7 @@ struct CascadeArgs {
   int64_t segs_per_block;
   double tie_eps;
   int single;            // 1: one pose through the latency kernel (cascade_single.cu)
+  int pdl;               // 1: launch with programmatic dependent launch (serial loop)
   // cross-block scratch and output
   double* partials;      // n_poses * blocks_per_pose * kNumMoments (if bpp > 1)
   unsigned* counters;    // n_poses, zero-initialised, re-armed by the kernel

@@ -491,6 +491,11 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     return;
   }
   GF_STAMP(3)
+  // Programmatic dependent launch (the serial loop): everything above -- the
+  // pose setup and the mode loop -- overlapped the previous query's tail;
+  // the partials and the ticket below are shared with it, so wait for that
+  // grid to complete (a no-op without a PDL launch).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // ---- cluster stage: ranks 1.. push their block moments to rank 0 through
   // distributed shared memory; rank 0 sums them in rank order (fixed)
   unsigned crank, csize;
@@ -575,6 +580,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? kMinBlocksLaunch : 
   // load of freshly written launch memory on the setup critical path
   if (threadIdx.x < 12)
     pose_s[threadIdx.x] = a.poses ? a.poses[a.pose_offset * 12 + threadIdx.x] : a.pose_inline[threadIdx.x];
+  // let the next query of a PDL launch sequence start its setup now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   cluster_red_init(cr);  // ends with __syncthreads
   single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, a.done_seq, blockIdx.x, gridDim.x);
 }
@@ -739,13 +746,16 @@ cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // serial loop: programmatic dependent launch (see griddepcontrol in the body)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, cascade3d_single_kernel<T, WRAP>, a);
 }
 

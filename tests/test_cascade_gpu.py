@@ -210,3 +210,27 @@ def test_cascade_3d_long_runs_launch_and_server(be, w, wrap, prec, tol):
             # a plain cooperative launch, whose cross-CTA sum has another
             # association -- equal to the last bits, not bit for bit
             np.testing.assert_allclose(s, g, rtol=0, atol=1e-14 * np.max(np.abs(g)))
+
+
+@pytest.mark.parametrize("w,prec", [(64, "fp32"), (32, "fp64"), (96, "fp32")])
+def test_serial_loop_matches_single_queries(be, w, prec):
+    """gf_cascade_serial (one launch per pose, programmatic dependent launch:
+    query i+1 starts under query i's tail) gives every pose exactly the bits
+    of a lone gf_cascade call -- the overlapped queries share the partials
+    and ticket, which they touch only after the previous grid completed."""
+    import torch
+
+    rng = np.random.default_rng(70 + w)
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom, dcell, c = (0.05,) * 3, 0.3, rng.normal(size=3)
+    n = 300
+    Rs = np.stack([random_rotation(rng) for _ in range(n)])
+    ts = rng.uniform(-1, 1, (n, 3))
+    poses = torch.from_numpy(be.pack_poses(Rs, ts)).cuda()
+    out = be.cascade_batch(W1, W2, False, dom, dcell, c, poses, precision=prec, serial=True)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.complex128)
+    for i in list(range(0, n, 37)) + [n - 1]:
+        want = be.cascade(W1, W2, False, dom, dcell, Rs[i], ts[i], c, precision=prec)
+        np.testing.assert_array_equal(got[i], want)
