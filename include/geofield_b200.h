@@ -209,6 +209,15 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double *domega, do
                     int precision, double idle_timeout_s, int max_sms, uint64_t *server_id);
 int gf_server_query(uint64_t server_id, const double *R, const double *t_eff, double *out);
 int gf_server_stop(uint64_t server_id);
+/* Diagnostics of the server's last query, microseconds (-1: not observed):
+ * out[0] host time from posting the request to reading the result, out[1]
+ * the GPU's detect -> result time (globaltimer), out[2] post -> detect and
+ * out[3] result -> host receipt (host realtime clock vs globaltimer: the two
+ * differ by a slowly drifting offset, so compare with a typical query),
+ * out[4] the host's time to post the request, out[5] the longest stretch
+ * between two mailbox polls of the GPU's polling warp, out[6] the longest
+ * stretch between two clock reads of a warp beside it (an SM stall). */
+int gf_server_last_timing(uint64_t server_id, double *out7);
 
 /* Experiment knobs: the batched sweep's run length along the run axis per
  * thread (0 = auto), and per-CTA phase timestamps (globaltimer ns) of the

@@ -74,6 +74,7 @@ SIGNATURES = {
                                        ctypes.c_int, ctypes.c_double, ctypes.c_int, c_u64p]),
     "gf_server_query": (ctypes.c_int, [ctypes.c_uint64, c_dp, c_dp, c_dp]),
     "gf_server_query_fast": (ctypes.c_int, [ctypes.c_uint64, c_vp, c_vp, c_vp]),
+    "gf_server_last_timing": (ctypes.c_int, [ctypes.c_uint64, c_dp]),
     "gf_server_stop": (ctypes.c_int, [ctypes.c_uint64]),
     "gf_set_cascade_run_length": (ctypes.c_int, [ctypes.c_int]),
 }

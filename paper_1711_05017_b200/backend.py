@@ -287,6 +287,16 @@ class HapticServer:
             self._c_ref, self._d_ref = center, domega
         return True
 
+    def last_timing(self):
+        """Timing of the last query in us (-1: not observed): host round trip,
+        GPU detect -> result, post -> GPU detect, GPU result -> host receipt.
+        A long round trip with a short GPU part locates the stall on the host
+        or the PCIe path, not in the grid."""
+        out = np.zeros(7)
+        check(LIB.gf_server_last_timing(self.id, dptr(out)))
+        return {"host_us": out[0], "gpu_us": out[1], "post_to_detect_us": out[2], "result_to_host_us": out[3],
+                "post_us": out[4], "gpu_poll_gap_us": out[5], "gpu_clock_gap_us": out[6]}
+
     def retire(self):
         """The device side has exited (idle timeout): stop routing calls here."""
         if _servers.get(self.key) is self:

@@ -587,6 +587,12 @@ struct Server {
   unsigned* counters = nullptr;
   unsigned long long seq = 0;
   bool running = false;
+  // the last query (gf_server_last_timing): host round trip, GPU detect ->
+  // result, post -> detect, result -> receipt (us; -1 when not observed)
+  // + post duration on the host, longest GPU stretch between two mailbox polls
+  // (and of a clock-only warp of the same CTA: an SM stall shows there too)
+  double last_timing[7] = {0.0, -1.0, -1.0, -1.0, 0.0, -1.0, -1.0};
+  long long last_post_rt = 0;
 };
 std::mutex g_srv_mu;
 std::unordered_map<uint64_t, std::unique_ptr<Server>> g_servers;
@@ -661,6 +667,8 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, do
   ctl.idle_timeout_ns = (unsigned long long)((idle_timeout_s > 0 ? idle_timeout_s : 30.0) * 1e9);
   ctl.sm_limit = max_sms > 0 ? max_sms : 1 << 30;
   ctl.enlist = s->counters + 2;
+  // detect time and poll gap: words 29, 30, past the 25 forwarded request slots
+  a.t_detect = reinterpret_cast<unsigned long long*>(s->dev_words) + 29;
   server_started();
   cudaError_t le = launch_cascade_server(a, ctl, s->stream);
   if (le != cudaSuccess) server_stopped();
@@ -679,10 +687,13 @@ int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, do
   GF_CHECK(s->running, GF_ESTOPPED, "server is not running (stopped or idle-timed out)");
   double pose[12];
   embed_pose(s->d, R, t_eff, pose);
+  auto t0 = std::chrono::steady_clock::now();
+  s->last_post_rt = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::system_clock::now().time_since_epoch()).count();
   post_request(s, pose, 0u);
+  const double post_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
   const unsigned long long seq = s->seq;
   double res[14];
-  auto t0 = std::chrono::steady_clock::now();
   int rc = wait_ll(s->mb->out, seq, res, [&]() -> int {
     cudaError_t e = cudaStreamQuery(s->stream);
     if (e != cudaErrorNotReady) {  // kernel exited (idle timeout) or failed
@@ -696,6 +707,30 @@ int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, do
     return 0;
   });
   if (rc) return rc;
+  // per-query timing: host post -> receipt, the GPU's detect -> result
+  // (globaltimer low words in tagged slots 28/29, written beside the results,
+  // briefly awaited) and -- on the realtime clock the globaltimer follows on
+  // this platform -- post -> detect and result -> receipt
+  const auto t1 = std::chrono::steady_clock::now();
+  const long long rt1 = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                            std::chrono::system_clock::now().time_since_epoch()).count();
+  s->last_timing[0] = std::chrono::duration<double, std::micro>(t1 - t0).count();
+  s->last_timing[1] = s->last_timing[2] = s->last_timing[3] = s->last_timing[5] = s->last_timing[6] = -1.0;
+  s->last_timing[4] = post_us;
+  for (int spin = 0; spin < 4096; ++spin) {
+    const unsigned long long d = s->mb->out[28], r = s->mb->out[29];
+    if ((unsigned)(d >> 32) == (unsigned)seq && (unsigned)(r >> 32) == (unsigned)seq) {
+      const unsigned det = (unsigned)d, res = (unsigned)r;
+      s->last_timing[1] = 1e-3 * (double)(unsigned)(res - det);
+      const unsigned post32 = (unsigned)(unsigned long long)s->last_post_rt, seen32 = (unsigned)(unsigned long long)rt1;
+      s->last_timing[2] = 1e-3 * (double)(int)(det - post32);
+      s->last_timing[3] = 1e-3 * (double)(int)(seen32 - res);
+      const unsigned long long gp = s->mb->out[30], cg = s->mb->out[31];
+      if ((unsigned)(gp >> 32) == (unsigned)seq) s->last_timing[5] = 1e-3 * (double)(gp & 0xffffffffull);
+      if ((unsigned)(cg >> 32) == (unsigned)seq) s->last_timing[6] = 1e-3 * (double)(cg & 0xffffffffull);
+      break;
+    }
+  }
   if (s->d == 3) {
     std::memcpy(out, res, 14 * sizeof(double));
   } else {
@@ -703,6 +738,13 @@ int gf_server_query(uint64_t server_id, const double* R, const double* t_eff, do
     out[6] = res[12];
     out[7] = res[13];
   }
+  return 0;
+}
+
+int gf_server_last_timing(uint64_t server_id, double* out7) {
+  Server* s = find_server(server_id);
+  GF_CHECK(s && out7, GF_EINVAL, "unknown server or null argument");
+  std::memcpy(out7, s->last_timing, sizeof s->last_timing);
   return 0;
 }
 

@@ -43,6 +43,9 @@ struct CascadeArgs {
   // completion word and the kernel no system-scope fence (or null: `out`).
   unsigned long long* ll_out;
   unsigned long long done_seq;  // tag of this query
+  // resident server only: globaltimer when the lead CTA saw the request; the
+  // finishing CTA reports (now - *t_detect) as a tagged 29th result slot
+  unsigned long long* t_detect;
 };
 
 // 26 moment accumulators (layout = the moment index order used by finalize)

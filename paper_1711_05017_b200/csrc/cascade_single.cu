@@ -155,6 +155,25 @@ __device__ __forceinline__ void emit_output(const CascadeArgs& a, int i, double 
   }
 }
 
+// Resident server: the low words of the globaltimer at request detection and
+// at the result, as tagged slots 28 and 29 -- per-frame diagnostics that
+// tell a slow GPU answer from a host or PCIe stall (the host stamps its own
+// post and receipt times beside them).
+__device__ __forceinline__ void emit_timing(const CascadeArgs& a, unsigned long long seq) {
+  if (!a.t_detect || !a.ll_out) return;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  const unsigned long long det = *(volatile unsigned long long*)a.t_detect;
+  const unsigned long long tag = (seq & 0xffffffffull) << 32;
+  const unsigned long long gap = *(volatile unsigned long long*)(a.t_detect + 1);
+  volatile unsigned long long* o = a.ll_out;
+  o[28] = tag | (det & 0xffffffffull);
+  o[29] = tag | (now & 0xffffffffull);
+  o[30] = tag | (gap > 0xffffffffull ? 0xffffffffull : gap);
+  const unsigned long long cgap = *(volatile unsigned long long*)(a.t_detect + 2);
+  o[31] = tag | (cgap > 0xffffffffull ? 0xffffffffull : cgap);
+}
+
 // One pose over all retained modes, spread across the grid; shared state is
 // passed in so the same body runs in the one-shot kernel and in the
 // persistent haptic server.  Non-final blocks return early (block-uniform).
@@ -488,6 +507,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   const int bpp = vg;
   if (bpp == 1) {
     if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
+    if (tid == 14) emit_timing(a, done_seq);
     return;
   }
   GF_STAMP(3)
@@ -563,6 +583,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   if (c < kNumMoments && s == 0) red[c] = part2;
   __syncthreads();
   if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
+  if (tid == 14) emit_timing(a, done_seq);
   if (tid == 0) a.counters[0] = 0u;
   GF_STAMP(5)
 }
@@ -677,13 +698,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_k
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         } while (t1 - t0 < (unsigned long long)(pw * 1000 / kPollWarps));
         mine = false;
+        unsigned long long t_prev = t1, gap = 0;  // longest stretch between two polls (diagnostics)
         while (true) {
-          if (lane < kReqSlots) v = ctl.host_req[lane];
+          // .cv: treat any cached copy of the system-memory line as stale and fetch again
+          if (lane < kReqSlots)
+            asm volatile("ld.global.cv.u64 %0, [%1];" : "=l"(v) : "l"(ctl.host_req + lane) : "memory");
           bool got = __all_sync(0xffffffffu, lane >= kReqSlots || (unsigned)(v >> 32) == expect);
           bool stop_now = false;
-          if (!got && pw == 0) {  // only warp 0 may give up on idleness
+          if (pw == 0) {  // only warp 0 may give up on idleness
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            stop_now = t1 - t0 > ctl.idle_timeout_ns;
+            gap = t1 - t_prev > gap ? t1 - t_prev : gap;
+            t_prev = t1;
+            stop_now = !got && t1 - t0 > ctl.idle_timeout_ns;
+            if (got && lane == 0) *(volatile unsigned long long*)(a.t_detect + 1) = gap;
           }
           if (got || stop_now) {
             int won = 0;
@@ -717,14 +744,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksServer) cascade3d_server_k
         if (lane < 12) pose_s[lane] = __hiloint2double((int)hi, (int)lo);
         if (lane == 0) cur = stopw ? kServerStop : last + 1;
       }
+    } else if (lead && tid >= 32 * kPollWarps && tid < 32 * (kPollWarps + 1)) {
+      // diagnostics: a warp that only reads the clock while the pollers wait --
+      // a long stretch here too means the SM stalled, not the PCIe read
+      unsigned long long tp, tn, gap = 0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp));
+      while (!*(volatile int*)&found) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+        gap = tn - tp > gap ? tn - tp : gap;
+        tp = tn;
+      }
+      if ((tid & 31) == 0) *(volatile unsigned long long*)(a.t_detect + 2) = gap;
     }
     __syncthreads();
     const unsigned long long sq = cur;
     if (sq == kServerStop) break;
-    if (a.debug && tid == 0) {  // when this CTA saw the query
+    if ((a.debug || lead) && tid == 0) {  // when this CTA saw the query
       unsigned long long t_;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-      a.debug[(int64_t)vb * 8 + 7] = t_;
+      if (a.debug) a.debug[(int64_t)vb * 8 + 7] = t_;
+      if (lead) *(volatile unsigned long long*)a.t_detect = t_;
     }
     single_pose_body<T, WRAP>(a, pose_s, sp, red, ticket, cr, smem_raw, sq, vb, vg);
     last = sq;

@@ -137,11 +137,11 @@ class HapticSession:
         if resident:
             from .energy import haptic_session
 
-            with haptic_session(self.fixed, self.moving, self.modes, max_sms=max_sms):
-                return self._run(rotations, translations, rate_hz, realtime)
+            with haptic_session(self.fixed, self.moving, self.modes, max_sms=max_sms) as srv:
+                return self._run(rotations, translations, rate_hz, realtime, srv)
         return self._run(rotations, translations, rate_hz, realtime)
 
-    def _run(self, rotations, translations, rate_hz, realtime=False):
+    def _run(self, rotations, translations, rate_hz, realtime=False, server=None):
         import gc
 
         period = 1.0 / rate_hz
@@ -149,7 +149,7 @@ class HapticSession:
         gc.disable()  # a collector pause inside the servo loop would be a missed frame
         restore = _enter_realtime() if realtime else None
         try:
-            out = self._paced(rotations, translations, period, rate_hz)
+            out = self._paced(rotations, translations, period, rate_hz, server)
             out["realtime"] = bool(restore and restore[2])
             return out
         finally:
@@ -158,7 +158,7 @@ class HapticSession:
             if gc_was:
                 gc.enable()
 
-    def _paced(self, rotations, translations, period, rate_hz):
+    def _paced(self, rotations, translations, period, rate_hz, server=None):
         """Servo pacing: sleep through most of the slack, spin only the last
         `_SPIN_S`.  A SCHED_FIFO thread that busy-waits the whole period uses
         100 % of its core and hits the kernel's real-time throttle
@@ -175,7 +175,10 @@ class HapticSession:
             if dt > period:
                 misses += 1
                 if len(late) < 16:
-                    late.append({"frame": i, "us": dt * 1e6, "start_lag_us": (t0 - t_next) * 1e6})
+                    rec = {"frame": i, "us": dt * 1e6, "start_lag_us": (t0 - t_next) * 1e6}
+                    if server is not None:  # where the time went: host, PCIe or the grid
+                        rec.update(server.last_timing())
+                    late.append(rec)
             t_next += period
             slack = t_next - time.perf_counter()
             if slack > _SPIN_S:
