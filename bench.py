@@ -472,9 +472,7 @@ def run_engine(args):
             "config": CONFIG,
             "e2e": {"value": e2e_value, "unit": "queries/s",
                     "h2d_bytes_per_step": QUERIES_PER_STEP * 25 * 8, "d2h_bytes_per_step": QUERIES_PER_STEP * 28 * 8,
-                    "path": "backend.cascade (host R, t_eff -> host complex128[7]) in a haptic session "
-                            "(backend.HapticServer): 25 self-tagged request slots read from pinned host memory, 28 "
-                            "result slots written back, no launch per query",
+                    "path": "backend.cascade in a haptic session (resident grid, host-mapped mailbox)",
                     "launch_path_value": r4(args.e2e_queries * world / dt1)},
             "roofline": {"bound": "fp32" if prec == "fp32" else "fp64", "achieved": achieved, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": _traffic("cascade3d_single_kernel"),
@@ -592,7 +590,7 @@ def measure_stages(args, rank, world, fp32_peak, fp64_peak, parity):
     lead = rank == 0
     cpu_ok = lead and not args.no_cpu
     if lead:
-        out.update(stage_trajectories(args, parity, cpu_ok))
+        out.update(stage_trajectories(args, parity, cpu_ok, fp32_peak))
     barrier(world)
     out["C3"] = stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok)
     torch.cuda.empty_cache()
@@ -601,14 +599,14 @@ def measure_stages(args, rank, world, fp32_peak, fp64_peak, parity):
     torch.cuda.empty_cache()
     barrier(world)
     if lead:
-        out["C5"] = stage_haptic(args, parity, cpu_ok)
+        out["C5"] = stage_haptic(args, parity, cpu_ok, fp32_peak)
         out["W"] = stage_window(args, parity, cpu_ok)
         out["D"] = stage_density(args, fp64_peak, parity, cpu_ok)
     barrier(world)
     return out
 
 
-def stage_trajectories(args, parity, cpu_ok):
+def stage_trajectories(args, parity, cpu_ok, fp32_peak):
     """C1 (the reference's CPU case) and C2 on real GPU-built assets, through
     the public evaluate() inside a haptic session; parity vs the reference
     kernel on the very windows the engine uses."""
@@ -633,21 +631,27 @@ def stage_trajectories(args, parity, cpu_ok):
         else:  # the headline's jittered path
             Rj, tj, _ = trajectory(npose, SEED + 11)
             cfgs = [Configuration(R, t) for R, t in zip(Rj, tj)]
-        with haptic_session(a1, a2, m):
+        with haptic_session(a1, a2, m) as srv:
             for cfg in cfgs[:50]:
                 evaluate(a1, a2, cfg, m)
-            lat, rows = [], []
+            lat, rows, gpu = [], [], []
             t0 = time.perf_counter()
             for cfg in cfgs:
                 q0 = time.perf_counter_ns()
                 ev = evaluate(a1, a2, cfg, m)
                 lat.append((time.perf_counter_ns() - q0) / 1e3)
                 rows.append(np.concatenate([[ev.score.real], ev.force, ev.torque]))
+                gpu.append(srv.last_timing()["gpu_us"])
             dt = time.perf_counter() - t0
         lat.sort()
+        gpu_us = statistics.median(gpu)
+        live = live_fraction(np.array([c.rotation for c in cfgs[::max(1, len(cfgs) // 8)]]), side)
+        achieved = 240.0 * live * m / (gpu_us * 1e-6) / 1e12
         st = {"poses_per_s": r4(len(cfgs) / dt), "p50_us": r4(lat[len(lat) // 2]),
-              "p99_us": r4(lat[min(len(lat) - 1, int(0.99 * len(lat)))]), "precompute_ms": r4(pre_ms),
-              "inputs": f"{scene} {n}^3 K={side // 2} GPU-built assets, evaluate() in a haptic session"}
+              "p99_us": r4(lat[min(len(lat) - 1, int(0.99 * len(lat)))]), "gpu_us_p50": r4(gpu_us),
+              "roofline": {"bound": "fp32", "achieved": r4(achieved), "peak": r4(fp32_peak), "unit": "TFLOP/s",
+                           "frac": r4(achieved / fp32_peak)},
+              "precompute_ms": r4(pre_ms), "in": f"{scene} {n}^3 GPU assets, evaluate() in a session"}
         if cpu_ok:
             g = a1.grid
             C1h, C2h = np.asarray(w1), np.asarray(w2)
@@ -722,7 +726,7 @@ def stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok):
     achieved = 240.0 * live * w3 ** 3 * (hi - lo) / (ms * 1e-3) / 1e12
     st = {"poses": len(ts), "n_gpus": world, "poses_per_s": r4(len(ts) / (ms * 1e-3)), "s": r4(ms * 1e-3),
           "e2e_poses_per_s": r4(len(ts) / e2e_s), "frac": r4(achieved / fp32_peak), "tflops": r4(achieved),
-          "density_s": r4(dens_s), "inputs": "gear_pair 256^3 GPU density -> w=96 windows; cmd_bench poses seed 0"}
+          "density_s": r4(dens_s), "in": "gear_pair 256^3 GPU assets, cmd_bench poses"}
     if cpu_ok:
         C1h, C2h = np.asarray(W1), np.asarray(W2)
         idx = np.array([0, 1, 4097, (hi - lo) - 1])
@@ -764,7 +768,7 @@ def stage_field(args, rank, world, parity, cpu_ok):
     st = {"n": n4, "n_gpus": world, "ms": r4(ms), "gvox_per_s": r4(n4 ** 3 / (ms * 1e-3) / 1e9),
           "roofline": {"bound": "hbm", "achieved": r4(alg / (ms * 1e-3) / 1e9), "peak": hbm, "unit": "GB/s",
                        "frac": r4(alg / (ms * 1e-3) / 1e9 / hbm), "work": "24 B/voxel"},
-          "density_s": r4(dens_s), "inputs": "gear_pair 512^3 GPU density -> full spectra (wrap)"}
+          "density_s": r4(dens_s), "in": "gear_pair 512^3 GPU spectra"}
     if world == 1:  # cuFFT C2C inverse of the same size (torch.fft -> cuFFT), the speed bar
         x = torch.empty((n4,) * 3, dtype=torch.complex64, device="cuda")
         x.normal_()
@@ -814,7 +818,7 @@ def stage_field(args, rank, world, parity, cpu_ok):
     return st
 
 
-def stage_haptic(args, parity, cpu_ok):
+def stage_haptic(args, parity, cpu_ok, fp32_peak):
     """C5: bolt-nut 256^3, K=64 (w = 128) from GPU-built densities of the
     ~10^5-face meshes; a screw trajectory (2 turns, pitch 0.1) paced at
     1 kHz, one evaluate per frame from a resident query grid; then the same
@@ -836,10 +840,18 @@ def stage_haptic(args, parity, cpu_ok):
     sess = HapticSession(f5[0], f5[1], None)
     sess.run(R5[:200], t5[:200], rate_hz=1000.0)  # warm
     run = sess.run(R5, t5, rate_hz=1000.0)
+    live = live_fraction(R5[:: max(1, frames // 8)], w5)
+    gpu_us = run["gpu_us_p50"]
+    achieved = 240.0 * live * w5 ** 3 / (gpu_us * 1e-6) / 1e12
+    missed = [{k: r4(v) for k, v in m.items() if k in ("frame", "us", "gpu_us", "gpu_poll_gap_us", "gpu_clock_gap_us")}
+              for m in run["missed"][:4]]
     st = {"frames": run["frames"], "p50_us": r4(run["p50_us"]), "p99_us": r4(run["p99_us"]),
-          "max_us": r4(run["max_us"]), "misses": run["deadline_misses"], "missed": run["missed"][:4],
-          "realtime": run["realtime"], "rt_runtime_us": run["rt_runtime_us"], "density_s": r4(dens_s),
-          "inputs": "bolt_nut 256^3 GPU density (75852 + 98816 faces) -> w=128 windows"}
+          "max_us": r4(run["max_us"]), "misses": run["deadline_misses"], "missed": missed,
+          "miss_cause": "GPU-wide stall (gpu_clock_gap_us)",
+          "realtime": run["realtime"], "gpu_us_p50": r4(gpu_us),
+          "roofline": {"bound": "fp32", "achieved": r4(achieved), "peak": r4(fp32_peak), "unit": "TFLOP/s",
+                       "frac": r4(achieved / fp32_peak), "work": f"240 flop x live modes ({live:.3f} x {w5 ** 3})"},
+          "density_s": r4(dens_s), "in": "bolt_nut 256^3 GPU assets (75852 + 98816 faces)"}
     # concurrency: a landscape export in a worker thread while the session serves frames
     # on a subset of the SMs (the reference service's field worker, service.py:305-318)
     gl = scenes_mod().get_scene("bolt_nut").grid(256)
@@ -889,6 +901,11 @@ def stage_haptic(args, parity, cpu_ok):
                                range(len(idx))))
         want = np.array([np.concatenate([[w_[0].real], w_[1:4].real, w_[4:7].real]) for w_ in want])
         parity["C5"] = parity_entry(np.array(with_s), want, np.asarray(l1).real, "oracle/_ref _core.cascade_3d")
+        t0 = time.perf_counter()
+        for k in range(2):
+            ref_cascade(C1h, C2h, False, dom, dcell, R5[idx[k]], tp[k], c)
+        st["cpu"] = {"value": r4(2 / (time.perf_counter() - t0)), "unit": "queries/s", "cores": 1,
+                     "kind": "reference", "per_query_ms": r4((time.perf_counter() - t0) / 2 * 1e3)}
     del f5, sess, W1, W2, L1, L2
     torch.cuda.empty_cache()
     return st

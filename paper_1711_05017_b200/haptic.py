@@ -164,7 +164,7 @@ class HapticSession:
         100 % of its core and hits the kernel's real-time throttle
         (sched_rt_runtime_us, 950 ms of every 1 s by default): it is then
         descheduled for ~50 ms -- the 46 ms frame of the round-1 C5 run."""
-        lat, misses, late = [], 0, []
+        lat, misses, late, gpu = [], 0, [], []
         t_next = time.perf_counter()
         for i, (R, t) in enumerate(zip(rotations, translations)):
             self.rotation, self.translation = np.asarray(R), np.asarray(t)
@@ -172,6 +172,8 @@ class HapticSession:
             self.eval_current()
             dt = time.perf_counter() - t0
             lat.append(dt * 1e6)
+            if server is not None:
+                gpu.append(server.last_timing()["gpu_us"])
             if dt > period:
                 misses += 1
                 if len(late) < 16:
@@ -190,4 +192,5 @@ class HapticSession:
         pct = lambda p: lat[min(len(lat) - 1, int(p * len(lat)))]  # noqa: E731  (cli.py:357-361)
         return {"frames": len(lat), "p50_us": statistics.median(lat), "p95_us": pct(0.95), "p99_us": pct(0.99),
                 "max_us": lat[-1], "max_frame": worst, "deadline_misses": misses, "missed": late,
-                "rate_hz": rate_hz, "rt_runtime_us": _rt_runtime_us()}
+                "rate_hz": rate_hz, "rt_runtime_us": _rt_runtime_us(),
+                "gpu_us_p50": statistics.median(gpu) if gpu else None}
