@@ -589,19 +589,38 @@ def measure_stages(args, rank, world, fp32_peak, fp64_peak, parity):
     out = {}
     lead = rank == 0
     cpu_ok = lead and not args.no_cpu
+
+    def guarded(key, fn, collective):
+        """A stage that fails records its error instead of ending the run (the
+        headline line still prints); for the sharded stages every rank learns
+        whether any rank failed, so none waits in a collective alone."""
+        err = None
+        try:
+            out[key] = fn()
+        except Exception as e:  # noqa: BLE001  (reported in the JSON line)
+            err = f"{type(e).__name__}: {e}"[:200]
+            out[key] = {"error": err}
+        torch.cuda.empty_cache()
+        if collective and world > 1:
+            flag = torch.tensor([1.0 if err else 0.0], device="cuda")
+            import torch.distributed as dist
+
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            return flag.item() == 0.0
+        return err is None
+
     if lead:
-        out.update(stage_trajectories(args, parity, cpu_ok, fp32_peak))
+        guarded("C1C2", lambda: stage_trajectories(args, parity, cpu_ok, fp32_peak), False)
+        out.update(out.pop("C1C2") if "error" not in out.get("C1C2", {}) else {"C1C2": out["C1C2"]})
     barrier(world)
-    out["C3"] = stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok)
-    torch.cuda.empty_cache()
-    barrier(world)
-    out["C4"] = stage_field(args, rank, world, parity, cpu_ok)
-    torch.cuda.empty_cache()
+    if guarded("C3", lambda: stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok), True):
+        barrier(world)
+        guarded("C4", lambda: stage_field(args, rank, world, parity, cpu_ok), True)
     barrier(world)
     if lead:
-        out["C5"] = stage_haptic(args, parity, cpu_ok, fp32_peak)
-        out["W"] = stage_window(args, parity, cpu_ok)
-        out["D"] = stage_density(args, fp64_peak, parity, cpu_ok)
+        guarded("C5", lambda: stage_haptic(args, parity, cpu_ok, fp32_peak), False)
+        guarded("W", lambda: stage_window(args, parity, cpu_ok), False)
+        guarded("D", lambda: stage_density(args, fp64_peak, parity, cpu_ok), False)
     barrier(world)
     return out
 
