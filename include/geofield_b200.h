@@ -183,6 +183,15 @@ int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double *domega, con
                    const double *s, double scale, int precision, void *work_dev, void *work2_dev, void *out_dev,
                    void *stream);
 
+/* Moment-spectrum rotational gradient (energy._rotational_gradient_vector,
+ * energy.py:210-251): the reference's independent cross-check of the torque
+ * from the moving part's centre-referenced moment windows hmom[0..d-1]
+ * (the windows of rho p_a).  out receives d_rot interleaved complex128
+ * values (3 in 3D, 1 in 2D; the rest zero), already 2 pi i dcell scaled.
+ * float64 throughout, one fused pass over the window. */
+int gf_vector_torque(uint64_t h1, uint64_t h2, const uint64_t *hmom, int wrap, const double *domega, double dcell,
+                     const double *R, const double *t_eff, const double *center, double *out);
+
 /* Diagnostics: FMA-pipe peak (TFLOP/s, 2 flops per FMA) measured with an
  * FMA-chain kernel on the current device; the roofline denominator of the
  * query/sweep kernels (precision 32 or 64). */

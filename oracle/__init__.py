@@ -643,3 +643,31 @@ def score_field_scale(C1, C2, wrap, dims, spacing, R, stride=1, chunk=1 << 22):
         total += float(np.sum(np.abs(C1[tuple(mesh)].ravel() * V)))
     dcell = 1.0 / (float(np.prod(dims)) * spacing ** d)
     return dcell * total * stride ** d
+
+
+def rotational_gradient_vector(C1, C2, moments, wrap, domega, dcell, R, t, center):
+    """Moment-spectrum rotational gradient: numpy restatement of
+    energy._rotational_gradient_vector (energy.py:210-251), the reference's
+    cross-check of the torque; `moments` are the centre-referenced windows
+    of rho p_a, `t` the configuration translation."""
+    C1 = np.asarray(C1)
+    d = C1.ndim
+    window = C1.shape
+    dom = np.asarray(domega, dtype=np.float64)
+    W = window_freqs(window, dom)
+    u = -(W @ R) / dom + np.asarray([w // 2 for w in window])
+    V, _ = interp_window(np.asarray(C2), u, wrap)
+    c = np.asarray(center, dtype=np.float64)
+    M = [-(interp_window(np.asarray(mw), u, wrap)[0]) + c[a] * V for a, mw in enumerate(moments)]
+    t_eff = np.asarray(t, dtype=np.float64) - c + R @ c
+    base = C1.ravel() * np.exp(2j * np.pi * (W @ t_eff))
+    gens = [np.array([[0.0, -1.0], [1.0, 0.0]])] if d == 2 else [
+        np.array([[0.0, 0.0, 0.0], [0.0, 0.0, -1.0], [0.0, 1.0, 0.0]]),
+        np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 0.0], [-1.0, 0.0, 0.0]]),
+        np.array([[0.0, -1.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 0.0]])]
+    out = []
+    for G in gens:
+        dirs = W @ (R.T @ G).T
+        samp = sum(dirs[:, a] * M[a] for a in range(d))
+        out.append(dcell * (2j * np.pi * np.sum(base * samp) + 2j * np.pi * np.sum(base * (W @ (G @ (R @ c))) * V)))
+    return np.asarray(out)

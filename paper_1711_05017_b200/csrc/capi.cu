@@ -359,6 +359,18 @@ int window_operands(uint64_t h1, uint64_t h2, int wrap, int precision, cudaStrea
   return 0;
 }
 
+// complex128 window h with its shape (vector_torque.cu)
+int window_raw64(uint64_t h, const void** raw, int w[3], int* dim) {
+  int rc = ensure_context();
+  if (rc) return rc;
+  Window* win = find_window(h);
+  GF_CHECK(win, GF_EINVAL, "unknown window handle");
+  *raw = win->raw64;
+  for (int a = 0; a < 3; ++a) w[a] = win->w[a];
+  *dim = win->d;
+  return 0;
+}
+
 }  // namespace gf
 
 using namespace gf;
