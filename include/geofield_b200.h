@@ -183,6 +183,15 @@ int gf_score_field(uint64_t h1, uint64_t h2, int wrap, const double *domega, con
                    const double *s, double scale, int precision, void *work_dev, void *work2_dev, void *out_dev,
                    void *stream);
 
+/* Elementwise steps between the heavy kernels (device buffers, stream-
+ * ordered): C *= exp(2 pi i w.s) over a DC-centred complex128 window in
+ * place, the phase summed over axes in float64 (spectral.center_window,
+ * spectral.py:184-195, with s = the grid centre); and the landscape's seam
+ * mask (energy._wrap_mask, energy.py:286-306) as OR of per-axis host flags
+ * (dims[0] + dims[1] (+ dims[2]) bytes) into one byte per node. */
+int gf_phase_window(void *data_c128, int d, const int32_t *w, const double *domega, const double *shift, void *stream);
+int gf_wrap_mask(uint8_t *mask_dev, int d, const int32_t *dims, const uint8_t *axis_flags, void *stream);
+
 /* Moment-spectrum rotational gradient (energy._rotational_gradient_vector,
  * energy.py:210-251): the reference's independent cross-check of the torque
  * from the moving part's centre-referenced moment windows hmom[0..d-1]

@@ -70,6 +70,8 @@ SIGNATURES = {
     "gf_score_field": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, c_i32p, c_dp, c_dp,
                                       ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
     "gf_set_cascade_debug": (ctypes.c_int, [c_vp]),
+    "gf_phase_window": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32p, c_dp, c_dp, c_vp]),
+    "gf_wrap_mask": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32p, c_u8p, c_vp]),
     "gf_vector_torque": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int,
                                         c_dp, ctypes.c_double, c_dp, c_dp, c_dp, c_dp]),
     "gf_server_start": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, c_dp, ctypes.c_double, c_dp,
