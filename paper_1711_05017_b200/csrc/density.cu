@@ -184,11 +184,13 @@ __global__ void __launch_bounds__(kThreads) dist_wind_kernel(PointSource src, co
 // D1a + D1b on grid nodes, culled (3D).  Same values and decisions as
 // dist_wind_kernel, with less work per node:
 //  * distance: the elements are also kept in a spatially sorted copy whose
-//    tiles carry a bounding sphere (centre, inflated radius).  A node's
-//    upper bound on its min distance is |p - c_t| + r_t of its nearest tile
-//    centre; a tile whose lower bound |p - c_t| - r_t exceeds that (with a
-//    1e-9 relative margin) cannot hold the minimum and is skipped.  The min
-//    is order-independent, so the value is the same bits as the full loop
+//    tiles carry a bounding sphere (centre, inflated radius) and one of
+//    their vertices.  A node's upper bound on its min distance is its
+//    distance to the nearest such vertex (a point of the surface), lowered
+//    to the running minimum as tiles are evaluated; a tile whose lower bound
+//    |p - c_t| - r_t exceeds it (1e-9 relative + 1e-12 coordinate-scale
+//    margin) cannot hold the minimum and is skipped.  The min is
+//    order-independent, so the value is the same bits as the full loop
 //    (the reference's BVH prunes the same way, _core.pyx:189-230).
 //  * winding: with `wind_bbox`, a node outside the (closed) mesh's inflated
 //    bounding box has winding number 0 up to rounding, so `inside` is false
@@ -199,7 +201,9 @@ __global__ void __launch_bounds__(kThreads) dist_wind_kernel(PointSource src, co
 struct CullInfo {
   const double* sorted;    // ne x 9, spatially ordered copy of the elements
   const double4* spheres;  // per kTile tile of `sorted`: centre xyz, radius
+  const double4* reps;     // per tile: one vertex of the tile (xyz)
   int ntiles;
+  double scale;            // max(1, |coordinate|) over the elements
   int wind_bbox;           // 1: winding only for nodes inside [lo, hi]
   double lo[3], hi[3];
 };
@@ -216,23 +220,20 @@ __global__ void __launch_bounds__(kThreads) dist_wind_culled_kernel(PointSource 
   const d3 pp = {p[0], p[1], p[2]};
   double best = 1e300;
   if (xi_out) {
-    // upper bound of the min distance from the nearest tile centre
-    double dmin2 = 1e300, rsel = 0.0;
+    // upper bound of the min distance: the nearest tile vertex
+    double ub2 = 1e300;
     for (int t = 0; t < ci.ntiles; ++t) {
-      const double4 s = ci.spheres[t];
-      const double dx = p[0] - s.x, dy = p[1] - s.y, dz = p[2] - s.z;
-      const double d2 = dx * dx + dy * dy + dz * dz;
-      if (d2 < dmin2) {
-        dmin2 = d2;
-        rsel = s.w;
-      }
+      const double4 v = ci.reps[t];
+      const double dx = p[0] - v.x, dy = p[1] - v.y, dz = p[2] - v.z;
+      ub2 = fmin(ub2, dx * dx + dy * dy + dz * dz);
     }
-    const double lim = (sqrt(dmin2) + rsel) * (1.0 + 1e-9);
+    const double ub = sqrt(ub2);
+    const double slack = 1e-12 * (fabs(p[0]) + fabs(p[1]) + fabs(p[2]) + ci.scale);
     for (int t = 0; t < ci.ntiles; ++t) {
       const double4 s = ci.spheres[t];
       const double dx = p[0] - s.x, dy = p[1] - s.y, dz = p[2] - s.z;
-      const double reach = lim + s.w;
-      const bool need = live && dx * dx + dy * dy + dz * dz <= reach * reach;
+      const double bound = fmin(ub, best) * (1.0 + 1e-9) + slack;
+      const bool need = live && sqrt(dx * dx + dy * dy + dz * dz) - s.w <= bound;
       if (!__syncthreads_or(need)) continue;
       const int64_t e0 = (int64_t)t * kTile;
       const int n = (int)min((int64_t)kTile, ne - e0);
@@ -279,27 +280,37 @@ struct SweepParams {
   int max_depth;
 };
 
-__device__ __forceinline__ void leaf_3d(const d3& a, const d3& b, const d3& c, double area, const d3& p,
-                                        const double* nrm, double xi, const SweepParams& sp, double& re, double& im,
-                                        int64_t& ncl) {
-  double mx = (a.x + b.x + c.x) / 3.0 - p.x;
-  double my = (a.y + b.y + c.y) / 3.0 - p.y;
-  double mz = (a.z + b.z + c.z) / 3.0 - p.z;
-  double eta = sqrt(mx * mx + my * my + mz * mz);
+// one leaf from its centroid offset m = centroid - p and eta = |m|.
+// The reference's four divisions (dot area / eta, eta / xi, / sigma, / den)
+// are regrouped into one: targ = (eta - xi) * xs with xs = 1 / (xi sigma)
+// per node, scale = gconst g dot area / (eta den).  The terms move by a few
+// ulps (the values are compared at 1e-12; every decision -- subdivision,
+// residual, clamp, exact-zero skip -- is taken on unchanged quantities).
+__device__ __forceinline__ void leaf_3d_c(double mx, double my, double mz, double eta, double area,
+                                          const double* nrm, double xi, double xs, const SweepParams& sp, double& re,
+                                          double& im, int64_t& ncl) {
   if (eta < sp.eta_min) {
     eta = sp.eta_min;
     ++ncl;
   }
-  double dot = mx * nrm[0] + my * nrm[1] + mz * nrm[2];
-  double dA = dot * area / eta;
-  double targ = (eta / xi - 1.0) / sp.sigma;
-  double g = exp(-0.5 * targ * targ) * sp.ginv;
-  double z2r = xi * xi - eta * eta;
-  double z2i = 2.0 * xi * eta;
-  double den = z2r * z2r + z2i * z2i;
-  double scale = sp.gconst * g * dA / den;
+  const double dot = mx * nrm[0] + my * nrm[1] + mz * nrm[2];
+  const double targ = (eta - xi) * xs;
+  const double g = exp(-0.5 * targ * targ) * sp.ginv;
+  const double z2r = xi * xi - eta * eta;
+  const double z2i = 2.0 * xi * eta;
+  const double den = z2r * z2r + z2i * z2i;
+  const double scale = sp.gconst * g * (dot * area) / (eta * den);
   re += scale * z2r;
   im -= scale * z2i;
+}
+
+__device__ __forceinline__ void leaf_3d(const d3& a, const d3& b, const d3& c, double area, const d3& p,
+                                        const double* nrm, double xi, double xs, const SweepParams& sp, double& re,
+                                        double& im, int64_t& ncl) {
+  const double mx = (a.x + b.x + c.x) / 3.0 - p.x;
+  const double my = (a.y + b.y + c.y) / 3.0 - p.y;
+  const double mz = (a.z + b.z + c.z) / 3.0 - p.z;
+  leaf_3d_c(mx, my, mz, sqrt(mx * mx + my * my + mz * mz), area, nrm, xi, xs, sp, re, im, ncl);
 }
 
 struct Tri { d3 a, b, c; };
@@ -324,16 +335,25 @@ __device__ __forceinline__ Tri child_tri(const Tri& P, int k) {
 // below max_angle (1e-9 margin), the reference's measure test
 // area / (dist^2 + 1e-300) > max_angle cannot fire, so the exact distance is
 // not needed -- the face is a leaf, with the same bits and no residual.
+// Exact zeros (3D): a leaf whose centroid distance eta exceeds
+// thr = xi (1 + 38.7 sigma) has |targ| > 38.7, exp(-targ^2 / 2) underflows to
+// +0 and its terms are +-0, which leave re and im unchanged bit for bit; such
+// a face is skipped after the depth-0 test, and a whole tile is skipped when
+// its sphere (`tiles`: centre, radius, largest measure) puts every centroid
+// beyond thr and every face through the depth-0 shortcut (no subdivision, no
+// residual).  Element centroids are staged once per tile with the
+// reference's expression ((a + b + c) / 3).
 template <int D>
 __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, const double* __restrict__ elems,
                                                               const double* __restrict__ normals,
                                                               const double* __restrict__ measures,
-                                                              const double* __restrict__ radii, int64_t ne, int64_t m,
+                                                              const double* __restrict__ radii,
+                                                              const double* __restrict__ tiles, int64_t ne, int64_t m,
                                                               const double* __restrict__ xi_eff, SweepParams sp,
                                                               double* __restrict__ out, double* __restrict__ resid,
                                                               int64_t* __restrict__ clamps) {
   constexpr int E = D == 3 ? 9 : 4;
-  constexpr int ET = E + D + 1 + (D == 3 ? 1 : 0);  // element + normal + measure (+ radius)
+  constexpr int ET = E + D + 1 + (D == 3 ? 4 : 0);  // element + normal + measure (+ radius, centroid)
   constexpr int kThreads = kSweepThreads;
   __shared__ double tile[kTile * ET];
   const int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x;
@@ -349,34 +369,53 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
   Tri frame[24];
   unsigned char taken[24];
 
+  const double thr = xi * (1.0 + 38.7 * sp.sigma) * (1.0 + 1e-9);
+  const double xs = 1.0 / (xi * sp.sigma);
+  const double pslack = 1e-12 * (fabs(p.x) + fabs(p.y) + fabs(p.z));
   for (int64_t e0 = 0; e0 < ne; e0 += kTile) {
     const int n = (int)min((int64_t)kTile, ne - e0);
-    __syncthreads();
+    bool need = live;
+    if (D == 3 && need) {
+      const double* ts = tiles + 5 * (e0 / kTile);
+      const double dx = p.x - ts[0], dy = p.y - ts[1], dz = p.z - ts[2];
+      const double lb = sqrt(dx * dx + dy * dy + dz * dz) - ts[3] - pslack;
+      need = !(lb > thr && ts[4] < sp.max_angle * (lb * lb) * (1.0 - 1e-9));
+    }
+    if (!__syncthreads_or(need)) continue;
     for (int t = threadIdx.x; t < n * E; t += kThreads) tile[(t / E) * ET + t % E] = elems[e0 * E + t];
     for (int t = threadIdx.x; t < n * D; t += kThreads) tile[(t / D) * ET + E + t % D] = normals[e0 * D + t];
     for (int t = threadIdx.x; t < n; t += kThreads) tile[t * ET + E + D] = measures[e0 + t];
     if (D == 3)
-      for (int t = threadIdx.x; t < n; t += kThreads) tile[t * ET + E + D + 1] = radii[e0 + t];
+      for (int t = threadIdx.x; t < n; t += kThreads) {
+        const double* g = elems + (e0 + t) * 9;
+        double* o = tile + t * ET + E + D + 1;
+        o[0] = radii[e0 + t];
+        o[1] = (g[0] + g[3] + g[6]) / 3.0;
+        o[2] = (g[1] + g[4] + g[7]) / 3.0;
+        o[3] = (g[2] + g[5] + g[8]) / 3.0;
+      }
     __syncthreads();
-    if (!live) continue;
-    for (int e = 0; e < n; ++e) {
+    if (need) for (int e = 0; e < n; ++e) {
       const double* q = tile + e * ET;
       const double* nrm = q + E;
       double meas = q[E + D];
       int depth = 0;
       constexpr int nchild = D == 3 ? 4 : 2;
       Tri cur;
-      if (D == 3) cur = Tri{{q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}};
-      else cur = Tri{{q[0], q[1], 0.0}, {q[2], q[3], 0.0}, {0.0, 0.0, 0.0}};
       if (D == 3) {  // far face: a depth-0 leaf without the exact distance (see above)
-        const double mx = (cur.a.x + cur.b.x + cur.c.x) / 3.0 - p.x;
-        const double my = (cur.a.y + cur.b.y + cur.c.y) / 3.0 - p.y;
-        const double mz = (cur.a.z + cur.b.z + cur.c.z) / 3.0 - p.z;
-        const double lb = sqrt(mx * mx + my * my + mz * mz) - q[E + D + 1];
+        const double mx = q[E + D + 2] - p.x;
+        const double my = q[E + D + 3] - p.y;
+        const double mz = q[E + D + 4] - p.z;
+        const double eta = sqrt(mx * mx + my * my + mz * mz);
+        const double lb = eta - q[E + D + 1];
         if (lb > 0.0 && meas < sp.max_angle * (lb * lb) * (1.0 - 1e-9)) {
-          leaf_3d(cur.a, cur.b, cur.c, meas, p, nrm, xi, sp, re, im, ncl);
+          if (eta > thr) continue;  // exact zero
+          leaf_3d_c(mx, my, mz, eta, meas, nrm, xi, xs, sp, re, im, ncl);
           continue;
         }
+        cur = Tri{{q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}};
+      } else {
+        cur = Tri{{q[0], q[1], 0.0}, {q[2], q[3], 0.0}, {0.0, 0.0, 0.0}};
       }
       while (true) {
         double measure;
@@ -403,7 +442,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
         }
         if (measure > sp.max_angle && measure > worst) worst = measure;
         if (D == 3) {
-          leaf_3d(cur.a, cur.b, cur.c, meas, p, nrm, xi, sp, re, im, ncl);
+          leaf_3d(cur.a, cur.b, cur.c, meas, p, nrm, xi, xs, sp, re, im, ncl);
         } else {
           double mx = 0.5 * (cur.a.x + cur.b.x) - p.x, my = 0.5 * (cur.a.y + cur.b.y) - p.y;
           double eta = sqrt(mx * mx + my * my);
@@ -612,10 +651,20 @@ int check_dim(int d) {
   return 0;
 }
 
-// Per-triangle bounding radius about the centroid (a + b + c) / 3, inflated
-// so rounding can only make it larger (the sweep's depth-0 shortcut).
-std::vector<double> triangle_radii(const double* el, int64_t ne) {
-  std::vector<double> r(ne);
+// Sweep aids of a triangle set, both inflated so rounding can only make them
+// larger: per-triangle bounding radius about the centroid (a + b + c) / 3
+// (the depth-0 shortcut), and per kTile tile of the ORIGINAL element order
+// (the sweep sums in that order) a bounding sphere of the tile's vertices
+// plus its largest measure: {cx, cy, cz, r, max measure} (the zero-tile cull).
+struct SweepAids {
+  std::vector<double> radii, tiles;
+};
+
+SweepAids sweep_aids(const double* el, const double* meas, int64_t ne) {
+  SweepAids s;
+  s.radii.resize(ne);
+  double scale = 1.0;
+  for (int64_t k = 0; k < 9 * ne; ++k) scale = std::max(scale, std::fabs(el[k]));
   for (int64_t e = 0; e < ne; ++e) {
     const double* q = el + 9 * e;
     const double c[3] = {(q[0] + q[3] + q[6]) / 3.0, (q[1] + q[4] + q[7]) / 3.0, (q[2] + q[5] + q[8]) / 3.0};
@@ -624,9 +673,36 @@ std::vector<double> triangle_radii(const double* el, int64_t ne) {
       const double dx = q[3 * v] - c[0], dy = q[3 * v + 1] - c[1], dz = q[3 * v + 2] - c[2];
       m = std::max(m, std::sqrt(dx * dx + dy * dy + dz * dz));
     }
-    r[e] = m * (1.0 + 1e-12) + 1e-300;
+    s.radii[e] = m * (1.0 + 1e-12) + 1e-300;
   }
-  return r;
+  const int64_t nt = ceil_div(ne, kTile);
+  s.tiles.resize(5 * nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t e1 = std::min(ne, (t + 1) * kTile);
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300}, mx = 0.0;
+    for (int64_t e = t * kTile; e < e1; ++e) {
+      mx = std::max(mx, meas[e]);
+      for (int k = 0; k < 9; ++k) {
+        lo[k % 3] = std::min(lo[k % 3], el[9 * e + k]);
+        hi[k % 3] = std::max(hi[k % 3], el[9 * e + k]);
+      }
+    }
+    const double c[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+    double r = 0.0;
+    for (int64_t e = t * kTile; e < e1; ++e)
+      for (int v = 0; v < 3; ++v) {
+        const double* q = el + 9 * e + 3 * v;
+        const double dx = q[0] - c[0], dy = q[1] - c[1], dz = q[2] - c[2];
+        r = std::max(r, std::sqrt(dx * dx + dy * dy + dz * dz));
+      }
+    double* o = &s.tiles[5 * t];
+    o[0] = c[0];
+    o[1] = c[1];
+    o[2] = c[2];
+    o[3] = r * (1.0 + 1e-12) + 1e-12 * scale;
+    o[4] = mx;
+  }
+  return s;
 }
 
 // Culling aids of a closed triangle set for dist_wind_culled_kernel: the
@@ -634,8 +710,8 @@ std::vector<double> triangle_radii(const double* el, int64_t ne) {
 // bounding sphere per tile, and the inflated bounding box.
 struct CullHost {
   std::vector<double> sorted;
-  std::vector<double4> spheres;
-  double lo[3], hi[3];
+  std::vector<double4> spheres;  // ntiles spheres, then ntiles representative vertices
+  double lo[3], hi[3], scale;
 };
 
 void build_cull(const double* el, int64_t ne, CullHost& h) {
@@ -665,8 +741,12 @@ void build_cull(const double* el, int64_t ne, CullHost& h) {
   h.sorted.resize(9 * ne);
   for (int64_t e = 0; e < ne; ++e) std::memcpy(&h.sorted[9 * e], el + 9 * key[e].second, 9 * sizeof(double));
   const int64_t nt = ceil_div(ne, kTile);
-  h.spheres.resize(nt);
+  h.spheres.resize(2 * nt);
+  h.scale = 1.0;
+  for (int64_t k = 0; k < 9 * ne; ++k) h.scale = std::max(h.scale, std::fabs(el[k]));
   for (int64_t t = 0; t < nt; ++t) {
+    const double* v0 = &h.sorted[9 * t * kTile];
+    h.spheres[nt + t] = make_double4(v0[0], v0[1], v0[2], 0.0);
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     const int64_t e1 = std::min(ne, (t + 1) * kTile);
     for (int64_t e = t * kTile; e < e1; ++e)
@@ -699,8 +779,10 @@ int upload_cull(const CullHost& h, int64_t ne, int wind_bbox, DevBuf& ds, DevBuf
   if (rc) return rc;
   if ((rc = upload(h.spheres.data(), sizeof(double4) * h.spheres.size(), dsp, st))) return rc;
   ci.sorted = (const double*)ds.p;
+  ci.ntiles = (int)(h.spheres.size() / 2);
   ci.spheres = (const double4*)dsp.p;
-  ci.ntiles = (int)h.spheres.size();
+  ci.reps = ci.spheres + ci.ntiles;
+  ci.scale = h.scale;
   ci.wind_bbox = wind_bbox;
   for (int a = 0; a < 3; ++a) {
     ci.lo[a] = h.lo[a];
@@ -800,19 +882,21 @@ int gf_sweep(int d, const double* elems, const double* normals, const double* me
   src.d = d;
   SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
   unsigned grid = (unsigned)ceil_div(m, kSweepThreads);
-  DevBuf drad;
-  std::vector<double> radii;
+  DevBuf drad, dtil;
   if (d == 3) {
-    radii = triangle_radii(elems, ne);
-    if ((rc = upload(radii.data(), sizeof(double) * ne, drad, st))) return rc;
+    const SweepAids aids = sweep_aids(elems, measures, ne);
+    if ((rc = upload(aids.radii.data(), sizeof(double) * ne, drad, st))) return rc;
+    if ((rc = upload(aids.tiles.data(), sizeof(double) * aids.tiles.size(), dtil, st))) return rc;
     sweep_kernel<3><<<grid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
-                                                    (const double*)dm.p, (const double*)drad.p, ne, m,
-                                                    (const double*)dx.p, sp, (double*)dout.p, (double*)dres.p,
-                                                    (int64_t*)dcl.p);
+                                                    (const double*)dm.p, (const double*)drad.p,
+                                                    (const double*)dtil.p, ne, m, (const double*)dx.p, sp,
+                                                    (double*)dout.p, (double*)dres.p, (int64_t*)dcl.p);
+    GF_CUDA(cudaStreamSynchronize(st));  // `aids` leaves scope
   } else {
     sweep_kernel<2><<<grid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
-                                                    (const double*)dm.p, nullptr, ne, m, (const double*)dx.p, sp,
-                                                    (double*)dout.p, (double*)dres.p, (int64_t*)dcl.p);
+                                                    (const double*)dm.p, nullptr, nullptr, ne, m,
+                                                    (const double*)dx.p, sp, (double*)dout.p, (double*)dres.p,
+                                                    (int64_t*)dcl.p);
   }
   GF_CUDA(cudaGetLastError());
   GF_CUDA(cudaMemcpyAsync(out_c128, dout.p, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, st));
@@ -887,8 +971,8 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     }
   } ev_guard{ev};
   GF_CUDA(cudaEventRecord(ev[0], st));
-  DevBuf dsorted, dspheres, drad;
-  std::vector<double> radii;
+  DevBuf dsorted, dspheres, drad, dtil;
+  SweepAids aids;  // (alive until the final synchronize)
   if (d == 3) {
     // winding values leave this pipeline only for the inverse-square family;
     // the skeletal family needs occupancy alone (the bounding-box shortcut)
@@ -898,8 +982,9 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     if ((rc = upload_cull(ch, ne, family != 0 ? 1 : 0, dsorted, dspheres, ci, st))) return rc;
     dist_wind_culled_kernel<<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, ci, (double*)dxi.p,
                                                        (double*)dwind.p);
-    radii = triangle_radii(elems, ne);
-    if ((rc = upload(radii.data(), sizeof(double) * ne, drad, st))) return rc;
+    aids = sweep_aids(elems, measures, ne);
+    if ((rc = upload(aids.radii.data(), sizeof(double) * ne, drad, st))) return rc;
+    if ((rc = upload(aids.tiles.data(), sizeof(double) * aids.tiles.size(), dtil, st))) return rc;
   } else {
     dist_wind_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dxi.p, (double*)dwind.p);
   }
@@ -914,13 +999,14 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     const unsigned sgrid = (unsigned)ceil_div(m, kSweepThreads);
     if (d == 3)
       sweep_kernel<3><<<sgrid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
-                                                       (const double*)dm.p, (const double*)drad.p, ne, m,
-                                                       (const double*)dxe.p, sp, (double*)dip.p, (double*)dres.p,
-                                                       (int64_t*)dcl.p);
+                                                       (const double*)dm.p, (const double*)drad.p,
+                                                       (const double*)dtil.p, ne, m, (const double*)dxe.p, sp,
+                                                       (double*)dip.p, (double*)dres.p, (int64_t*)dcl.p);
     else
       sweep_kernel<2><<<sgrid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
-                                                       (const double*)dm.p, nullptr, ne, m, (const double*)dxe.p, sp,
-                                                       (double*)dip.p, (double*)dres.p, (int64_t*)dcl.p);
+                                                       (const double*)dm.p, nullptr, nullptr, ne, m,
+                                                       (const double*)dxe.p, sp, (double*)dip.p, (double*)dres.p,
+                                                       (int64_t*)dcl.p);
     GF_CUDA(cudaGetLastError());
   }
   GF_CUDA(cudaEventRecord(ev[2], st));
