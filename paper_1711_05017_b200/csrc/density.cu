@@ -137,6 +137,20 @@ struct PointSource {
       p[1] = node_coord(origin[1], spacing, j);
     }
   }
+  // node visited by thread slot g: row-major, or (3D grid nodes whose (y, z)
+  // plane tiles by BY x BZ) BY x BZ patches of one plane, so a block's nodes
+  // are spatially compact and its culling decisions agree
+  template <int BY, int BZ>
+  __device__ __forceinline__ int64_t node_of(int64_t g) const {
+    if (P || d != 3 || dims[1] % BY || dims[2] % BZ) return g;
+    const int64_t pn = (int64_t)dims[1] * dims[2];
+    const int64_t plane = g / pn;
+    const int r = (int)(g - plane * pn);
+    const int t = r % (BY * BZ), b = r / (BY * BZ);
+    const int nbz = dims[2] / BZ;
+    const int j = (b / nbz) * BY + t / BZ, k = (b % nbz) * BZ + t % BZ;
+    return plane * pn + (int64_t)j * dims[2] + k;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -213,8 +227,10 @@ __global__ void __launch_bounds__(kThreads) dist_wind_culled_kernel(PointSource 
                                                                     double* __restrict__ xi_out,
                                                                     double* __restrict__ wind_out) {
   __shared__ double tile[kTile * 9];
-  const int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x;
-  const bool live = i < m;
+  static_assert(kThreads == 16 * 8, "brick shape");
+  const int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x;
+  const bool live = g < m;
+  const int64_t i = live ? src.node_of<16, 8>(g) : g;
   double p[3] = {0.0, 0.0, 0.0};
   if (live) src.get(i, p);
   const d3 pp = {p[0], p[1], p[2]};
@@ -356,8 +372,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
   constexpr int ET = E + D + 1 + (D == 3 ? 4 : 0);  // element + normal + measure (+ radius, centroid)
   constexpr int kThreads = kSweepThreads;
   __shared__ double tile[kTile * ET];
-  const int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x;
-  const bool live = i < m;
+  static_assert(kThreads == 16 * 16, "brick shape");
+  const int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x;
+  const bool live = g < m;
+  const int64_t i = live ? src.node_of<16, 16>(g) : g;
   double p3[3] = {0.0, 0.0, 0.0};
   if (live) src.get(i, p3);
   const d3 p = {p3[0], p3[1], p3[2]};
