@@ -108,6 +108,15 @@ __device__ __forceinline__ double exact_u_s(const double* R, const double* dom, 
   return __dadd_rn(__ddiv_rn(-s, dom[a]), (double)ha);
 }
 
+// A_g[ax][bb] = (Omega_g R)[ax][bb] for row-major R, Omega_g the generator
+// of rotations about axis g: -eps(g, ax, c) R[c][bb] with c the third axis
+// (0 when g == ax) -- selects, no lane-divergent branches in the setup
+__device__ __forceinline__ double gen_rot(const double* R, int g, int ax, int bb) {
+  const int c = 3 - g - ax;
+  const double v = R[3 * ((unsigned)c > 2u ? 0 : c) + bb];
+  return g == ax ? 0.0 : ((ax - g + 3) % 3 == 1 ? -v : v);
+}
+
 // tie-table floor stored in the real slot: as raw int bits for fp32 (no
 // int<->float conversion in the mode loop), as a value for fp64
 __device__ __forceinline__ float pack_floor(int v, float) { return __int_as_float(v); }
@@ -212,24 +221,13 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   }
   if (tid >= 32 && tid < 32 + 27) {  // A_g = Omega_g R (_core.pyx:615-626)
     const int k = tid - 32, g = k / 9, bb = (k / 3) % 3, ax = k % 3;
-    const double* Rr = src;  // row-major R
-    double Aab;  // A_g[ax][bb]
-    if (g == 0) Aab = ax == 0 ? 0.0 : (ax == 1 ? -Rr[6 + bb] : Rr[3 + bb]);
-    else if (g == 1) Aab = ax == 0 ? Rr[6 + bb] : (ax == 1 ? 0.0 : -Rr[bb]);
-    else Aab = ax == 0 ? -Rr[3 + bb] : (ax == 1 ? Rr[bb] : 0.0);
-    sp.cg[g][bb][ax] = -Aab * a.rdom[ax][bb];
+    sp.cg[g][bb][ax] = -gen_rot(src, g, ax, bb) * a.rdom[ax][bb];
   }
   if (tid >= 64 && tid < 64 + 9) {  // q_g = A_g c
     const int g = (tid - 64) / 3, ax = (tid - 64) % 3;
-    const double* Rr = src;
     double q = 0.0;
-    for (int bb = 0; bb < 3; ++bb) {
-      double Aab;
-      if (g == 0) Aab = ax == 0 ? 0.0 : (ax == 1 ? -Rr[6 + bb] : Rr[3 + bb]);
-      else if (g == 1) Aab = ax == 0 ? Rr[6 + bb] : (ax == 1 ? 0.0 : -Rr[bb]);
-      else Aab = ax == 0 ? -Rr[3 + bb] : (ax == 1 ? Rr[bb] : 0.0);
-      q += Aab * a.center[bb];
-    }
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) q += gen_rot(src, g, ax, bb) * a.center[bb];
     sp.kq[g][ax] = a.dom[ax] * q;
   }
   if (tid >= 96 && tid < 99) sp.kt[tid - 96] = a.dom[tid - 96];
@@ -356,6 +354,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     cx<T> rX[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
     cx<T> rXJ[3] = {mk<T>(0, 0), mk<T>(0, 0), mk<T>(0, 0)};
     int c1off = (kx0 * w1 + ky0) * w2 + kz0;
+#pragma unroll(sizeof(T) == 4 ? 2 : 1)
     for (int kr = kr0; kr < kend; ++kr, c1off += sr) {
       const T j = (T)(kr - kr0);
       int il[3];
@@ -426,17 +425,22 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
         }
       }
       int ix = il[0], iy = il[1], iz = il[2];
+      bool inside = true;
       if (WRAP) {
         ix = ix < 0 ? ix + w0 : (ix >= w0 ? ix - w0 : ix);
         iy = iy < 0 ? iy + w1 : (iy >= w1 ? iy - w1 : iy);
         iz = iz < 0 ? iz + w2 : (iz >= w2 ? iz - w2 : iz);
       } else if ((unsigned)(ix + 1) > (unsigned)w0 || (unsigned)(iy + 1) > (unsigned)w1 ||
                  (unsigned)(iz + 1) > (unsigned)w2) {
-        continue;  // whole footprint outside the window: exact zero contribution
+        // whole footprint outside the window: an exact zero contribution.
+        // Predicated rather than skipped (base = 0 below, loads from a valid
+        // cell), so the unrolled loop can issue the next modes' loads early.
+        inside = false;
+        ix = iy = iz = -1;
       }
       const P4* ptr = C2 + ((ix + 1) * sx + (iy + 1) * sy + (iz + 1));
       P4 e00 = ldg_pair(ptr), e10 = ldg_pair(ptr + sx), e01 = ldg_pair(ptr + sy), e11 = ldg_pair(ptr + sx + sy);
-      const cx<T> base = C1[c1off] * (ph_pq * pt_r[kr]);
+      const cx<T> base = inside ? C1[c1off] * (ph_pq * pt_r[kr]) : mk<T>(0, 0);
       const T fu = f[0], fv = f[1], fs = f[2];
       cx<T> c000 = mk<T>(e00.x, e00.y), c001 = mk<T>(e00.z, e00.w);
       cx<T> c100 = mk<T>(e10.x, e10.y), c101 = mk<T>(e10.z, e10.w);
