@@ -27,6 +27,28 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
+def _ext_path():
+    import sysconfig
+
+    return os.path.join(HERE, "_gf_fast" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pyfast(force=False):
+    """The CPython binding of the per-frame session query (csrc/pyfast.c),
+    built with the host C compiler against this interpreter and numpy."""
+    import sysconfig
+
+    import numpy
+
+    src, out = os.path.join(HERE, "csrc", "pyfast.c"), _ext_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) > os.path.getmtime(src):
+        return out
+    cc = os.environ.get("CC", "gcc")
+    subprocess.run([cc, "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+                    "-I", numpy.get_include(), "-o", out, src], check=True)
+    return out
+
+
 def needs_build():
     if not os.path.exists(OUT):
         return True
@@ -42,6 +64,7 @@ NO_FMA = {"density.cu"}
 
 
 def build(verbose=False, force=False):
+    build_pyfast(force)
     if not force and not needs_build():
         return OUT
     from concurrent.futures import ThreadPoolExecutor

@@ -26,6 +26,13 @@ import numpy as np
 from . import _lib
 from ._lib import LIB, check, dptr
 
+try:  # CPython binding of the per-frame session query (csrc/pyfast.c); ctypes otherwise
+    from . import _gf_fast
+
+    _gf_fast.bind(ctypes.cast(LIB.gf_server_query_fast, ctypes.c_void_p).value)
+except ImportError:
+    _gf_fast = None
+
 HAVE_CORE = True  # the CUDA engine is the only (and compiled) backend
 
 _NAMES = ("cuda", "core")
@@ -188,16 +195,21 @@ def cascade(C1, C2, wrap, domega, dcell, R, t_eff, center, precision=None):
     bits = 64 if (precision or _precision) == "fp64" else 32
     if _servers and d == 3:
         # session path: only the pose travels (the server holds centre and
-        # domega); the per-call work is two buffer copies and one C call
+        # domega); one C call reads R and t_eff in place (_gf_fast), or two
+        # buffer copies and a ctypes call for operands it cannot read
         srv = _servers.get((W1.handle, W2.handle, bool(wrap), bits))
         if srv is not None and srv.dcell == dcell and srv.matches(center, domega):
-            q.R33[...] = R
-            q.t3[...] = t_eff
-            rc = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
-            if rc == 0:
-                return q.res3.copy()
-            if rc != _lib.ESTOPPED:
-                check(rc)
+            r = _gf_fast.server_query(srv.id, R, t_eff) if _gf_fast is not None else None
+            if r.__class__ is np.ndarray:
+                return r
+            if r is None:
+                q.R33[...] = R
+                q.t3[...] = t_eff
+                r = LIB.gf_server_query_fast(srv.id, q.pR, q.pt, q.pout)
+                if r == 0:
+                    return q.res3.copy()
+            if r != _lib.ESTOPPED:
+                check(r)
             srv.retire()  # idle-timed out: this and later calls take the launch path
     arg = q.arg
     if d == 3:

@@ -34,6 +34,24 @@ def test_header_symbols_exported_and_bound():
         assert target in syms
 
 
+def test_session_binding_loads_and_checks_operands():
+    # csrc/pyfast.c: the per-frame session query binding shares the ctypes
+    # library instance; operands it cannot read in place return None (the
+    # caller then takes the ctypes path), engine errors come back as the code
+    fast = backend._gf_fast
+    assert fast is not None, "_gf_fast extension not built (paper_1711_05017_b200/_build.py build_pyfast)"
+    R, t = np.eye(3), np.zeros(3)
+    assert fast.server_query(0, R.astype(np.float32), t) is None
+    assert fast.server_query(0, R, np.zeros(4)) is None
+    assert fast.server_query(0, R.T, t) is None  # not C-contiguous
+    assert fast.server_query(0, [[1.0, 0, 0]] * 3, t) is None
+    rc = fast.server_query(0, R, t)  # no such server
+    assert isinstance(rc, int) and rc == _lib.LIB.gf_server_query(0, R.ravel().ctypes.data_as(_lib.c_dp),
+                                                                   t.ctypes.data_as(_lib.c_dp),
+                                                                   np.zeros(14).ctypes.data_as(_lib.c_dp))
+    assert rc != 0
+
+
 def test_library_reports_missing_device_loudly():
     if os.environ.get("CUDA_VISIBLE_DEVICES", "") == "" and not _cuda_available():
         rc = _lib.LIB.gf_init(0)
