@@ -639,6 +639,7 @@ def stage_trajectories(args, parity, cpu_ok, fp32_peak):
                                                                               2000)):
         sc = scenes_mod().get_scene(scene)
         m = side ** 3
+        sc.build_assets(n, m_prime=m)  # warm-up: first use of the density / spectral kernels
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         a1, a2 = sc.build_assets(n, m_prime=m)

@@ -464,7 +464,7 @@ int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double 
     rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, c.stream);
     if (rc) return rc;
     a.poses = nullptr;
-    plan_cascade(a, 1, 2 * sm_count());
+    plan_cascade(a, 1, kLaunchCtasPerSm * sm_count());
     rc = ensure_scratch(c, (int64_t)a.blocks_per_pose * kNumMoments, 1, c.stream);
     if (rc) return rc;
     a.partials = c.partials;
@@ -558,7 +558,7 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   CascadeArgs a;
   rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, st);
   if (rc) return rc;
-  plan_cascade(a, 1, 2 * sm_count());
+  plan_cascade(a, 1, kLaunchCtasPerSm * sm_count());
   StreamScratch sc;
   rc = scratch_acquire((int64_t)a.blocks_per_pose * kNumMoments, 1, st, sc);
   if (rc) return rc;
@@ -657,7 +657,7 @@ int gf_server_start(uint64_t h1, uint64_t h2, int wrap, const double* domega, do
   rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, s->stream);
   if (rc) return rc;
   GF_CHECK(max_sms >= 0, GF_EINVAL, "max_sms must be >= 0 (0: every SM)");
-  plan_cascade(a, 1, 2 * sm_count());
+  plan_cascade(a, 1, kServerCtasPerSm * sm_count());
   GF_CHECK(a.single == 1, GF_EINTERNAL, "single-pose plan expected");
   GF_CUDA(cudaHostAlloc((void**)&s->mb, sizeof(Mailbox), cudaHostAllocMapped));
   std::memset((void*)s->mb, 0, sizeof(Mailbox));

@@ -471,7 +471,7 @@ void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks) {
 
   if (n_poses == 1) {
     a.single = 1;
-    a.blocks_per_pose = single_blocks(a, target_blocks / 2);
+    a.blocks_per_pose = single_blocks(a, target_blocks);
     return;
   }
   a.single = 0;

@@ -87,7 +87,14 @@ struct ServerCtl {
 };
 cudaError_t launch_cascade_server(const CascadeArgs& a, const ServerCtl& ctl, cudaStream_t st);
 
-int single_blocks(const CascadeArgs& a, int sms);
+// Grid of the single-pose kernels (measured, profiles/r02_cascade_grid.txt):
+// the lone query and the serial loop run one CTA per SM -- a programmatic
+// dependent launch's CTAs then fit beside the previous query's (serial loop
+// w = 64: 4.8 us/query against 6.7 at two per SM); the resident server, whose
+// queries cannot overlap, runs two per SM (7.9 us against 9.1 at one).
+constexpr int kLaunchCtasPerSm = 1;
+constexpr int kServerCtasPerSm = 2;
+int single_blocks(const CascadeArgs& a, int target_blocks);
 cudaError_t launch_cascade_single(const CascadeArgs& a, cudaStream_t st);
 void plan_cascade(CascadeArgs& a, int64_t n_poses, int target_blocks);
 cudaError_t launch_cascade(const CascadeArgs& a, int64_t n_poses, cudaStream_t st);

@@ -59,13 +59,12 @@ struct SinglePose {
 constexpr int kMaxCluster = 8;
 static_assert(kCluster <= kMaxCluster, "cluster stage sized for kMaxCluster ranks");
 // resident CTAs per SM the register budget is sized for: the server grid is
-// 2 x 148 CTAs (up to 128 registers); the one-shot kernel keeps room for a
-// third so the next launch's CTAs can start beside the previous tail
-constexpr int kMinBlocksServer = 2;
-#ifndef GF_LAUNCH_MINB
-#define GF_LAUNCH_MINB 3
-#endif
-constexpr int kMinBlocksLaunch = GF_LAUNCH_MINB;
+// kServerCtasPerSm x 148 CTAs (up to 128 registers); the one-shot kernel runs
+// kLaunchCtasPerSm per SM and keeps room for three (<= 80 registers), so the
+// CTAs of the next two launches of a PDL chain start beside the previous
+// tail (cascade.cuh)
+constexpr int kMinBlocksServer = kServerCtasPerSm;
+constexpr int kMinBlocksLaunch = 3;
 struct ClusterRed {
   double gather[kMaxCluster][kNumMoments];
   unsigned long long bar;
@@ -804,7 +803,7 @@ cudaError_t launch_single_t(const CascadeArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-int single_blocks(const CascadeArgs& a, int sms) {
+int single_blocks(const CascadeArgs& a, int target_blocks) {
   // units = nP * nQ * w_r, bounded by the orientation-independent worst case
   int64_t best = 0;
   for (int r = 0; r < 3; ++r) {
@@ -812,7 +811,7 @@ int single_blocks(const CascadeArgs& a, int sms) {
     int64_t u = ceil_div(a.w[o1], 16) * ceil_div(a.w[o2], 16) * a.w[r];
     if (best == 0 || u < best) best = u;
   }
-  const int64_t target = (int64_t)sms * 2;  // 2 CTAs per SM: one resident wave, measured best (profiles/r01_cascade_notes.md)
+  const int64_t target = target_blocks;
   // equal work per CTA: the largest count <= target that gives every CTA the
   // same number of units (no straggler CTA with one extra unit)
   int64_t b = best < target ? best : target;

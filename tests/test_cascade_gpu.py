@@ -188,7 +188,11 @@ def test_haptic_server_sm_budget(be, max_sms):
 def test_cascade_3d_long_runs_launch_and_server(be, w, wrap, prec, tol):
     """Windows large enough that every CTA walks several run-axis segments
     (the segment loop's fold and its segment boundaries): launch path vs the
-    oracle, and the resident server vs the launch path (bit for bit in fp32)."""
+    oracle, and the resident server vs the launch path.  The server grid has
+    two CTAs per SM, the launch grid one (cascade.cuh kServerCtasPerSm /
+    kLaunchCtasPerSm): the modes are split differently, so the cross-CTA sums
+    associate differently -- equal to the last bits of each precision, and
+    both within the oracle tolerance above."""
     rng = np.random.default_rng(5000 + w)
     C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
     W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
@@ -201,15 +205,12 @@ def test_cascade_3d_long_runs_launch_and_server(be, w, wrap, prec, tol):
         assert np.all(parity_tol(g, want, l1, tol)), (g, want, l1)
     with be.HapticServer(W1, W2, wrap, dom, dcell, c, precision=prec):
         srv = [be.cascade(W1, W2, wrap, dom, dcell, R, t, c, precision=prec) for R, t in poses]
-    for s, g in zip(srv, got):
-        if prec == "fp32":
-            np.testing.assert_array_equal(s, g)
-        else:
-            # fp64 at w=96: the cooperative server grid may be refused its
-            # 4-CTA clusters (62 KB of shared memory per CTA) and fall back to
-            # a plain cooperative launch, whose cross-CTA sum has another
-            # association -- equal to the last bits, not bit for bit
-            np.testing.assert_allclose(s, g, rtol=0, atol=1e-14 * np.max(np.abs(g)))
+    for s, g, (R, t) in zip(srv, got, poses):
+        l1 = oracle.cascade_term_scales(C1, C2, wrap, dom, dcell, R, t, c)
+        # per output: a bound on the re-association error of the fixed-order
+        # sums, (summation depth ~ 30) x eps x the term scale (L1 of |terms|)
+        k = 1e-5 if prec == "fp32" else 1e-13
+        assert np.all(np.abs(s - g) <= k * l1), (s, g, l1)
 
 
 @pytest.mark.parametrize("w,prec", [(64, "fp32"), (32, "fp64"), (96, "fp32")])
