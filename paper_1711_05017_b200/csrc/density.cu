@@ -294,39 +294,51 @@ __global__ void __launch_bounds__(kThreads) dist_wind_culled_kernel(PointSource 
 struct SweepParams {
   double sigma, gconst, max_angle, eta_min, ginv;
   int max_depth;
+  double max_angle_lo;  // max_angle (1 - 1e-9): the margin of the depth-0 shortcut
 };
+
+// 1 / x to about an ulp for normal positive x: the MUFU seed and two Newton steps
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
 
 // one leaf from its centroid offset m = centroid - p and eta = |m|.
 // The reference's four divisions (dot area / eta, eta / xi, / sigma, / den)
-// are regrouped into one: targ = (eta - xi) * xs with xs = 1 / (xi sigma)
-// per node, scale = gconst g dot area / (eta den).  The terms move by a few
-// ulps (the values are compared at 1e-12; every decision -- subdivision,
-// residual, clamp, exact-zero skip -- is taken on unchanged quantities).
+// and its exp are regrouped: g = exp2(-(eta - xi)^2 gk) with
+// gk = log2(e) / (2 (xi sigma)^2) per node, scale = gconst g dot area times a
+// Newton reciprocal of eta den.  The terms move by a few ulps (the values are
+// compared at 1e-12; every decision -- subdivision, residual, clamp,
+// exact-zero skip -- is taken on unchanged quantities).
 __device__ __forceinline__ void leaf_3d_c(double mx, double my, double mz, double eta, double area,
-                                          const double* nrm, double xi, double xs, const SweepParams& sp, double& re,
+                                          const double* nrm, double xi, double gk, const SweepParams& sp, double& re,
                                           double& im, int64_t& ncl) {
   if (eta < sp.eta_min) {
     eta = sp.eta_min;
     ++ncl;
   }
   const double dot = mx * nrm[0] + my * nrm[1] + mz * nrm[2];
-  const double targ = (eta - xi) * xs;
-  const double g = exp(-0.5 * targ * targ) * sp.ginv;
+  const double dd = eta - xi;
+  const double g = exp2(-(dd * dd) * gk) * sp.ginv;
   const double z2r = xi * xi - eta * eta;
   const double z2i = 2.0 * xi * eta;
   const double den = z2r * z2r + z2i * z2i;
-  const double scale = sp.gconst * g * (dot * area) / (eta * den);
+  const double scale = sp.gconst * g * (dot * area) * rcp_nr(eta * den);
   re += scale * z2r;
   im -= scale * z2i;
 }
 
 __device__ __forceinline__ void leaf_3d(const d3& a, const d3& b, const d3& c, double area, const d3& p,
-                                        const double* nrm, double xi, double xs, const SweepParams& sp, double& re,
+                                        const double* nrm, double xi, double gk, const SweepParams& sp, double& re,
                                         double& im, int64_t& ncl) {
   const double mx = (a.x + b.x + c.x) / 3.0 - p.x;
   const double my = (a.y + b.y + c.y) / 3.0 - p.y;
   const double mz = (a.z + b.z + c.z) / 3.0 - p.z;
-  leaf_3d_c(mx, my, mz, sqrt(mx * mx + my * my + mz * mz), area, nrm, xi, xs, sp, re, im, ncl);
+  leaf_3d_c(mx, my, mz, sqrt(mx * mx + my * my + mz * mz), area, nrm, xi, gk, sp, re, im, ncl);
 }
 
 struct Tri { d3 a, b, c; };
@@ -388,7 +400,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
   unsigned char taken[24];
 
   const double thr = xi * (1.0 + 38.7 * sp.sigma) * (1.0 + 1e-9);
-  const double xs = 1.0 / (xi * sp.sigma);
+  const double gk = 0.7213475204444817 / ((xi * sp.sigma) * (xi * sp.sigma));
   const double pslack = 1e-12 * (fabs(p.x) + fabs(p.y) + fabs(p.z));
   for (int64_t e0 = 0; e0 < ne; e0 += kTile) {
     const int n = (int)min((int64_t)kTile, ne - e0);
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
       const double* ts = tiles + 5 * (e0 / kTile);
       const double dx = p.x - ts[0], dy = p.y - ts[1], dz = p.z - ts[2];
       const double lb = sqrt(dx * dx + dy * dy + dz * dz) - ts[3] - pslack;
-      need = !(lb > thr && ts[4] < sp.max_angle * (lb * lb) * (1.0 - 1e-9));
+      need = !(lb > thr && ts[4] < sp.max_angle_lo * (lb * lb));
     }
     if (!__syncthreads_or(need)) continue;
     for (int t = threadIdx.x; t < n * E; t += kThreads) tile[(t / E) * ET + t % E] = elems[e0 * E + t];
@@ -426,9 +438,9 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
         const double mz = q[E + D + 4] - p.z;
         const double eta = sqrt(mx * mx + my * my + mz * mz);
         const double lb = eta - q[E + D + 1];
-        if (lb > 0.0 && meas < sp.max_angle * (lb * lb) * (1.0 - 1e-9)) {
+        if (lb > 0.0 && meas < sp.max_angle_lo * (lb * lb)) {
           if (eta > thr) continue;  // exact zero
-          leaf_3d_c(mx, my, mz, eta, meas, nrm, xi, xs, sp, re, im, ncl);
+          leaf_3d_c(mx, my, mz, eta, meas, nrm, xi, gk, sp, re, im, ncl);
           continue;
         }
         cur = Tri{{q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}};
@@ -460,7 +472,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
         }
         if (measure > sp.max_angle && measure > worst) worst = measure;
         if (D == 3) {
-          leaf_3d(cur.a, cur.b, cur.c, meas, p, nrm, xi, xs, sp, re, im, ncl);
+          leaf_3d(cur.a, cur.b, cur.c, meas, p, nrm, xi, gk, sp, re, im, ncl);
         } else {
           double mx = 0.5 * (cur.a.x + cur.b.x) - p.x, my = 0.5 * (cur.a.y + cur.b.y) - p.y;
           double eta = sqrt(mx * mx + my * my);
@@ -898,7 +910,8 @@ int gf_sweep(int d, const double* elems, const double* normals, const double* me
   PointSource src = {};
   src.P = (const double*)dp.p;
   src.d = d;
-  SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
+  SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth,
+                      max_angle * (1.0 - 1e-9)};
   unsigned grid = (unsigned)ceil_div(m, kSweepThreads);
   DevBuf drad, dtil;
   if (d == 3) {
@@ -1013,7 +1026,8 @@ int gf_affinity_planes(int d, const double* elems, const double* normals, const 
     GF_CUDA(dxe.alloc(sizeof(double) * m));
     clamp_min_kernel<<<sm_count() * 8, 256, 0, st>>>((const double*)dxi.p, (double*)dxe.p, m, eta_min);
     GF_CUDA(cudaGetLastError());
-    SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth};
+    SweepParams sp = {sigma, gconst, max_angle, eta_min, 1.0 / (2.5066282746310002 * sigma), max_depth,
+                      max_angle * (1.0 - 1e-9)};
     const unsigned sgrid = (unsigned)ceil_div(m, kSweepThreads);
     if (d == 3)
       sweep_kernel<3><<<sgrid, kSweepThreads, 0, st>>>(src, (const double*)de.p, (const double*)dn.p,
