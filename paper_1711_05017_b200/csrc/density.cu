@@ -314,22 +314,23 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // Newton reciprocal of eta den.  The terms move by a few ulps (the values are
 // compared at 1e-12; every decision -- subdivision, residual, clamp,
 // exact-zero skip -- is taken on unchanged quantities).
-__device__ __forceinline__ void leaf_3d_c(double mx, double my, double mz, double eta, double area,
-                                          const double* nrm, double xi, double gk, const SweepParams& sp, double& re,
-                                          double& im, int64_t& ncl) {
+__device__ __forceinline__ void leaf_3d_c(double mx, double my, double mz, double eta, double area, double n0,
+                                          double n1, double n2, double xi, double gk, const SweepParams& sp,
+                                          double& re, double& im, int64_t& ncl) {
   if (eta < sp.eta_min) {
     eta = sp.eta_min;
     ++ncl;
   }
-  const double dot = mx * nrm[0] + my * nrm[1] + mz * nrm[2];
+  // value arithmetic with explicit FMAs (this file is built -fmad=false for the decisions)
+  const double dot = __fma_rn(mz, n2, __fma_rn(my, n1, mx * n0));
   const double dd = eta - xi;
   const double g = exp2(-(dd * dd) * gk) * sp.ginv;
-  const double z2r = xi * xi - eta * eta;
-  const double z2i = 2.0 * xi * eta;
-  const double den = z2r * z2r + z2i * z2i;
+  const double z2r = __fma_rn(-eta, eta, xi * xi);
+  const double z2i = (2.0 * xi) * eta;
+  const double den = __fma_rn(z2r, z2r, z2i * z2i);
   const double scale = sp.gconst * g * (dot * area) * rcp_nr(eta * den);
-  re += scale * z2r;
-  im -= scale * z2i;
+  re = __fma_rn(scale, z2r, re);
+  im = __fma_rn(-scale, z2i, im);
 }
 
 __device__ __forceinline__ void leaf_3d(const d3& a, const d3& b, const d3& c, double area, const d3& p,
@@ -338,7 +339,7 @@ __device__ __forceinline__ void leaf_3d(const d3& a, const d3& b, const d3& c, d
   const double mx = (a.x + b.x + c.x) / 3.0 - p.x;
   const double my = (a.y + b.y + c.y) / 3.0 - p.y;
   const double mz = (a.z + b.z + c.z) / 3.0 - p.z;
-  leaf_3d_c(mx, my, mz, sqrt(mx * mx + my * my + mz * mz), area, nrm, xi, gk, sp, re, im, ncl);
+  leaf_3d_c(mx, my, mz, sqrt(mx * mx + my * my + mz * mz), area, nrm[0], nrm[1], nrm[2], xi, gk, sp, re, im, ncl);
 }
 
 struct Tri { d3 a, b, c; };
@@ -381,9 +382,12 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
                                                               double* __restrict__ out, double* __restrict__ resid,
                                                               int64_t* __restrict__ clamps) {
   constexpr int E = D == 3 ? 9 : 4;
-  constexpr int ET = E + D + 1 + (D == 3 ? 4 : 0);  // element + normal + measure (+ radius, centroid)
+  // tile record: 3D [centroid 3 | radius | measure | normal 3 | vertices 9 | pad], 144 bytes, so the
+  // depth-0 path reads its eight values as four 16-byte loads; 2D [segment 4 | normal 2 | measure]
+  constexpr int ET = D == 3 ? 18 : 7;
+  constexpr int OV = D == 3 ? 8 : 0, ON = D == 3 ? 5 : 4, OM = D == 3 ? 4 : 6;
   constexpr int kThreads = kSweepThreads;
-  __shared__ double tile[kTile * ET];
+  __shared__ __align__(16) double tile[kTile * ET];
   static_assert(kThreads == 16 * 16, "brick shape");
   const int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x;
   const bool live = g < m;
@@ -412,38 +416,43 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(PointSource src, c
       need = !(lb > thr && ts[4] < sp.max_angle_lo * (lb * lb));
     }
     if (!__syncthreads_or(need)) continue;
-    for (int t = threadIdx.x; t < n * E; t += kThreads) tile[(t / E) * ET + t % E] = elems[e0 * E + t];
-    for (int t = threadIdx.x; t < n * D; t += kThreads) tile[(t / D) * ET + E + t % D] = normals[e0 * D + t];
-    for (int t = threadIdx.x; t < n; t += kThreads) tile[t * ET + E + D] = measures[e0 + t];
+    for (int t = threadIdx.x; t < n * E; t += kThreads) tile[(t / E) * ET + OV + t % E] = elems[e0 * E + t];
+    for (int t = threadIdx.x; t < n * D; t += kThreads) tile[(t / D) * ET + ON + t % D] = normals[e0 * D + t];
+    for (int t = threadIdx.x; t < n; t += kThreads) tile[t * ET + OM] = measures[e0 + t];
     if (D == 3)
       for (int t = threadIdx.x; t < n; t += kThreads) {
         const double* g = elems + (e0 + t) * 9;
-        double* o = tile + t * ET + E + D + 1;
-        o[0] = radii[e0 + t];
-        o[1] = (g[0] + g[3] + g[6]) / 3.0;
-        o[2] = (g[1] + g[4] + g[7]) / 3.0;
-        o[3] = (g[2] + g[5] + g[8]) / 3.0;
+        double* o = tile + t * ET;
+        o[0] = (g[0] + g[3] + g[6]) / 3.0;
+        o[1] = (g[1] + g[4] + g[7]) / 3.0;
+        o[2] = (g[2] + g[5] + g[8]) / 3.0;
+        o[3] = radii[e0 + t];
       }
     __syncthreads();
     if (need) for (int e = 0; e < n; ++e) {
       const double* q = tile + e * ET;
-      const double* nrm = q + E;
-      double meas = q[E + D];
+      const double* nrm = q + ON;
+      double meas = q[OM];
       int depth = 0;
       constexpr int nchild = D == 3 ? 4 : 2;
       Tri cur;
       if (D == 3) {  // far face: a depth-0 leaf without the exact distance (see above)
-        const double mx = q[E + D + 2] - p.x;
-        const double my = q[E + D + 3] - p.y;
-        const double mz = q[E + D + 4] - p.z;
+        const double2 c01 = *reinterpret_cast<const double2*>(q);
+        const double2 c2r = *reinterpret_cast<const double2*>(q + 2);
+        const double2 mn0 = *reinterpret_cast<const double2*>(q + 4);
+        const double2 n12 = *reinterpret_cast<const double2*>(q + 6);
+        const double mx = c01.x - p.x;
+        const double my = c01.y - p.y;
+        const double mz = c2r.x - p.z;
         const double eta = sqrt(mx * mx + my * my + mz * mz);
-        const double lb = eta - q[E + D + 1];
+        const double lb = eta - c2r.y;
         if (lb > 0.0 && meas < sp.max_angle_lo * (lb * lb)) {
           if (eta > thr) continue;  // exact zero
-          leaf_3d_c(mx, my, mz, eta, meas, nrm, xi, gk, sp, re, im, ncl);
+          leaf_3d_c(mx, my, mz, eta, mn0.x, mn0.y, n12.x, n12.y, xi, gk, sp, re, im, ncl);
           continue;
         }
-        cur = Tri{{q[0], q[1], q[2]}, {q[3], q[4], q[5]}, {q[6], q[7], q[8]}};
+        const double* v = q + OV;
+        cur = Tri{{v[0], v[1], v[2]}, {v[3], v[4], v[5]}, {v[6], v[7], v[8]}};
       } else {
         cur = Tri{{q[0], q[1], 0.0}, {q[2], q[3], 0.0}, {0.0, 0.0, 0.0}};
       }
