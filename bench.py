@@ -762,7 +762,7 @@ def stage_sweep(args, rank, world, fp32_peak, parity, cpu_ok):
 
 def stage_field(args, rank, world, parity, cpu_ok):
     """C4: the full translational field at 512^3 (full spectra, w = N, wrap)
-    of the gear pair, one cmd_bench rotation (seed 1); slab-decomposed across
+    of the gear pair, one cmd_bench rotation (seed 1) and R = I; slab-decomposed across
     ranks when world > 1.  Roofline 24 B/voxel; cuFFT C2C
     of the same size timed beside it as the speed bar; parity on the m' =
     128^3 windowed variant's voxels against the C restatement of the cascade."""
@@ -789,6 +789,17 @@ def stage_field(args, rank, world, parity, cpu_ok):
           "roofline": {"bound": "hbm", "achieved": r4(alg / (ms * 1e-3) / 1e9), "peak": hbm, "unit": "GB/s",
                        "frac": r4(alg / (ms * 1e-3) / 1e9 / hbm), "work": "24 B/voxel"},
           "density_s": r4(dens_s), "in": "gear_pair 512^3 GPU spectra"}
+    # the survey's second rotation, R = I (lattice-aligned: every index comes from the tie tables)
+    if world > 1:
+        fi = lambda: parallel.score_field_slab(a1, a2, np.eye(3), None, precision=32)  # noqa: E731
+    else:
+        fi = lambda: score_field_device(a1, a2, np.eye(3), None, precision=32)  # noqa: E731
+    fi()
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_i = max_over_ranks(_time_ms(fi), world)
+    st["identity_R"] = {"ms": r4(ms_i), "gvox_per_s": r4(n4 ** 3 / (ms_i * 1e-3) / 1e9),
+                        "frac": r4(alg / (ms_i * 1e-3) / 1e9 / hbm)}
     if world == 1:  # cuFFT C2C inverse of the same size (torch.fft -> cuFFT), the speed bar
         x = torch.empty((n4,) * 3, dtype=torch.complex64, device="cuda")
         x.normal_()

@@ -118,6 +118,22 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
     c1v[h] = mk<T>(1, 0);
     if (a.C1 && kxl < a.nkx && ky < w1 && kz < w2) c1v[h] = C1[((int64_t)(a.kx0 + kxl) * w1 + ky) * w2 + kz];
   }
+  // fp32 indices: the 32.32 fixed-point u of this thread's first mode, the
+  // second (4 further along the slowest lane axis) by one exact 64-bit add
+  long long u0[3] = {0, 0, 0};
+  if constexpr (sizeof(T) == 4) {
+    const int o_f = t & 7, o_m = (t >> 3) & 7, o_s = t >> 6;
+    const int ox = pf == 0 ? o_f : (pm == 0 ? o_m : o_s);
+    const int oy = pf == 1 ? o_f : (pm == 1 ? o_m : o_s);
+    const int oz = pf == 2 ? o_f : (pm == 2 ? o_m : o_s);
+    const int kk[3] = {a.kx0 + bx * 8 + ox - hx, by * 8 + oy - hy, bz * 8 + oz - hz};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax)
+      if ((ax < 2 || a.dim == 3 ? a.tie_dep[ax] : -1) < 0)  // the axes the loop below reads from u
+        u0[ax] = ((long long)(ax == 0 ? hx : (ax == 1 ? hy : hz)) << 32) + (long long)kk[0] * a.ufix[ax][0] +
+                 (long long)kk[1] * a.ufix[ax][1] + (long long)kk[2] * a.ufix[ax][2];
+  }
+  const int ps = 3 - pf - pm;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int o_f = t & 7, o_m = (t >> 3) & 7, o_s = (t >> 6) + 4 * h;
@@ -130,25 +146,20 @@ __global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
     const int kk[3] = {kx - hx, ky - hy, kz - hz};
     T fl[3], f[3];
     if constexpr (sizeof(T) == 4) {
-      unsigned lo[3];
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
-        const long long u = ((long long)(ax == 0 ? hx : (ax == 1 ? hy : hz)) << 32) +
-                            (long long)kk[0] * a.ufix[ax][0] + (long long)kk[1] * a.ufix[ax][1] +
-                            (long long)kk[2] * a.ufix[ax][2];
-        lo[ax] = fix_lo(u);
-        fl[ax] = (T)fix_floor(u);
-        f[ax] = fix_frac(lo[ax]);
-      }
-#pragma unroll
-      for (int ax = 0; ax < 3; ++ax) {
-        if (!(ax < 2 || a.dim == 3)) continue;
-        const int dep = a.tie_dep[ax];
+        const int dep = ax < 2 || a.dim == 3 ? a.tie_dep[ax] : -1;
         if (dep >= 0) {  // lattice-aligned axis: tabulated reference floor / frac
           const cx<T> e = tt[dep][dep == 0 ? ox : (dep == 1 ? oy : oz)];
           fl[ax] = e.re;
           f[ax] = e.im;
-        } else if (fix_tie(lo[ax])) {
+          continue;
+        }
+        const long long u = u0[ax] + (h ? 4 * a.ufix[ax][ps] : 0);
+        const unsigned lo = fix_lo(u);
+        fl[ax] = (T)fix_floor(u);
+        f[ax] = fix_frac(lo);
+        if ((ax < 2 || a.dim == 3) && fix_tie(lo)) {
           double ue = exact_u_f(a.R, a.dom, ax, kx, ky, kz, hx, hy, hz, ax == 0 ? hx : (ax == 1 ? hy : hz));
           double fe = floor(ue);
           fl[ax] = (T)fe;
