@@ -559,18 +559,26 @@ int gf_cascade_serial(uint64_t h1, uint64_t h2, int wrap, const double* domega, 
   rc = fill_args(a, w1, w2, wrap, domega, dcell, center, precision, st);
   if (rc) return rc;
   plan_cascade(a, 1, kLaunchCtasPerSm * sm_count());
+  // one single-query launch per pose, stream-ordered (the haptic loop shape),
+  // chained by programmatic dependent launch: query i+1's CTAs start under
+  // query i's tail.  The cross-CTA scratch is a ring of kSerialSlots sets
+  // (partials, ticket, release word); query i uses slot i % kSerialSlots and
+  // waits only for that slot's previous user, so up to three queries (the
+  // CTAs that fit per SM) are in flight at once.
+  constexpr int kSerialSlots = 4;
+  constexpr int kWordStride = 32;  // ticket / release words 128 bytes apart
+  const int64_t pstride = (int64_t)a.blocks_per_pose * kNumMoments;
   StreamScratch sc;
-  rc = scratch_acquire((int64_t)a.blocks_per_pose * kNumMoments, 1, st, sc);
+  rc = scratch_acquire(kSerialSlots * pstride, 2 * kSerialSlots * kWordStride, st, sc);
   if (rc) return rc;
-  a.partials = sc.partials;
-  a.counters = sc.counters;
-  // one single-query launch per pose, stream-ordered (the haptic loop shape);
-  // programmatic dependent launch lets query i+1's pose setup and mode loop
-  // run under query i's reduction tail -- its shared-scratch stage still
-  // waits for query i to complete (griddepcontrol.wait)
   a.pdl = 1;
   cudaError_t le = cudaSuccess;
   for (int64_t i = 0; i < n && le == cudaSuccess; ++i) {
+    const int slot = (int)(i % kSerialSlots);
+    a.partials = sc.partials + slot * pstride;
+    a.counters = sc.counters + slot * kWordStride;
+    a.slot_done = sc.counters + (kSerialSlots + slot) * kWordStride;
+    a.slot_need = (unsigned)(i / kSerialSlots);
     a.poses = poses_dev + 12 * i;
     a.out = out_dev + 14 * i;
     le = launch_cascade(a, 1, st);

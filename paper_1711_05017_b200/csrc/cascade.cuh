@@ -35,6 +35,12 @@ struct CascadeArgs {
   // cross-block scratch and output
   double* partials;      // n_poses * blocks_per_pose * kNumMoments (if bpp > 1)
   unsigned* counters;    // n_poses, zero-initialised, re-armed by the kernel
+  // serial loop scratch ring (null: one scratch set, guarded by griddepcontrol.wait):
+  // this query's slot may be written once *slot_done >= slot_need (every
+  // earlier user of the slot has read it back); the finishing CTA then
+  // publishes slot_need + 1
+  unsigned* slot_done;
+  unsigned slot_need;
   double* out;           // n_poses * 14 (interleaved complex128 x 7)
   unsigned long long* debug;  // optional per-block phase timestamps (single kernel)
   // single kernel, host-polled result: 28 host-mapped 8-byte slots, slot 2i+h

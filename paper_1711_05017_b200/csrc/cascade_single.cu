@@ -182,6 +182,27 @@ __device__ __forceinline__ void emit_timing(const CascadeArgs& a, unsigned long 
   o[31] = tag | (cgap > 0xffffffffull ? 0xffffffffull : cgap);
 }
 
+// Serial-loop scratch ring (CascadeArgs::slot_done): wait until every earlier
+// user of this query's slot has published its release (one poller, then the
+// CTA barrier orders the slot writes after its acquire).
+__device__ __forceinline__ void ring_slot_acquire(const CascadeArgs& a, int tid) {
+  if (tid == 32) {
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.slot_done) : "memory");
+      if (v >= a.slot_need) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// ring mode: a query's grid completes only after its predecessor's, so work
+// stream-ordered after the chain sees every query finished
+__device__ __forceinline__ void ring_exit(bool ring) {
+  if (ring) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // One pose over all retained modes, spread across the grid; shared state is
 // passed in so the same body runs in the one-shot kernel and in the
 // persistent haptic server.  Non-final blocks return early (block-uniform).
@@ -507,18 +528,23 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   if (c < kNumMoments && s == 0) red[c] = part;
   __syncthreads();
 
+  // Programmatic dependent launch (the serial loop).  One scratch set: the
+  // partials and ticket below are shared with the previous query, so wait for
+  // its grid to complete here (everything above -- pose setup, mode loop --
+  // overlapped its tail; a no-op without a PDL launch).  Scratch ring
+  // (a.slot_done): the previous queries use other slots, so only this slot's
+  // last user is awaited, at the partials store; the grid-completion wait
+  // moves to the exit (ring_exit), which keeps the stream order of the chain.
+  const bool ring = a.slot_done != nullptr;
   const int bpp = vg;
   if (bpp == 1) {
     if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
     if (tid == 14) emit_timing(a, done_seq);
+    ring_exit(ring);
     return;
   }
   GF_STAMP(3)
-  // Programmatic dependent launch (the serial loop): everything above -- the
-  // pose setup and the mode loop -- overlapped the previous query's tail;
-  // the partials and the ticket below are shared with it, so wait for that
-  // grid to complete (a no-op without a PDL launch).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!ring) asm volatile("griddepcontrol.wait;" ::: "memory");
   // ---- cluster stage: ranks 1.. push their block moments to rank 0 through
   // distributed shared memory; rank 0 sums them in rank order (fixed)
   unsigned crank, csize;
@@ -539,8 +565,10 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
       if (tid == 0)
         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(map_rank0(smem_addr(&cr.bar)))
                      : "memory");
+      ring_exit(ring);
       return;
     }
+    double v = 0.0;
     if (tid < kNumMoments) {
       const unsigned bar = smem_addr(&cr.bar), par = cr.parity;
       unsigned done = 0;
@@ -550,14 +578,16 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
             : "=r"(done)
             : "r"(bar), "r"(par)
             : "memory");
-      double v = red[tid];
+      v = red[tid];
       for (unsigned r = 1; r < csize; ++r) v += cr.gather[r][tid];
-      a.partials[(int64_t)tid * nclusters + cid] = v;  // moment-major
     }
+    if (ring) ring_slot_acquire(a, tid);  // ends with __syncthreads
+    if (tid < kNumMoments) a.partials[(int64_t)tid * nclusters + cid] = v;  // moment-major
     __syncthreads();
     if (tid == 0) cr.parity ^= 1u;
-  } else if (tid < kNumMoments) {
-    a.partials[(int64_t)tid * nclusters + cid] = red[tid];
+  } else {
+    if (ring) ring_slot_acquire(a, tid);
+    if (tid < kNumMoments) a.partials[(int64_t)tid * nclusters + cid] = red[tid];
   }
   // ---- grid stage: integer ticket with release/acquire ordering
   __syncthreads();
@@ -567,7 +597,10 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   }
   __syncthreads();
   GF_STAMP(4)
-  if (ticket != (unsigned)(nclusters - 1)) return;
+  if (ticket != (unsigned)(nclusters - 1)) {
+    ring_exit(ring);
+    return;
+  }
   // last leader: 26 moments x 8 segments, independent loads, fixed order
   double part2 = 0.0;
   if (c < kNumMoments) {
@@ -587,8 +620,13 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   __syncthreads();
   if (tid < 14) emit_output(a, tid, finalize_slot(a, sp, red, tid), done_seq);
   if (tid == 14) emit_timing(a, done_seq);
-  if (tid == 0) a.counters[0] = 0u;
+  if (tid == 0) {
+    a.counters[0] = 0u;
+    if (ring)  // the slot's partials are read (the barrier above) and its ticket re-armed
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.slot_done), "r"(a.slot_need + 1u) : "memory");
+  }
   GF_STAMP(5)
+  ring_exit(ring);
 }
 
 template <typename T, bool WRAP>
