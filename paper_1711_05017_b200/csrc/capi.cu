@@ -469,8 +469,8 @@ int gf_cascade(uint64_t h1, uint64_t h2, int wrap, const double* domega, double 
     if (rc) return rc;
     a.partials = c.partials;
     a.counters = c.counters;
-    // lone-query kernel: self-tagged result slots; other plans (non-default
-    // variants): plain doubles into the same mapped buffer + stream sync
+    // lone-query kernel: self-tagged result slots; the batched plan (never
+    // chosen for one pose): plain doubles into the same mapped buffer + sync
     a.ll_out = a.single ? c.dev_out_alias : nullptr;
     a.out = a.single ? nullptr : reinterpret_cast<double*>(c.dev_out_alias);
     c.cargs = a;

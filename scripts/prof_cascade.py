@@ -12,8 +12,6 @@ prec = sys.argv[3] if len(sys.argv) > 3 else "fp32"
 rng = np.random.default_rng(0)
 from paper_1711_05017_b200 import _lib
 _lib.ensure_device(0)
-_lib.check(_lib.LIB.gf_set_cascade_variant(int(os.environ.get('VARIANT','1'))))
-_lib.check(_lib.LIB.gf_set_cascade_tile(int(os.environ.get('TILE','0'))))
 C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
 W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
 dom = (1.0 / (2 * w * 0.05),) * 3
