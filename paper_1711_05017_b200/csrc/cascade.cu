@@ -171,11 +171,15 @@ __global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
   if (tid < 32) load_pose(a, pose, ps);
   __syncthreads();
   if (tid == 0) {
-    // run axis r: smallest |R[b][2]| (equal spacing: C2-z component of mode axis b)
+    // run axis r: smallest |R[b][2]| (equal spacing: C2-z component of mode
+    // axis b), but never z: a run along C1's contiguous axis puts the 32 lanes
+    // of every C1 load on 32 different lines (measured +3.5-4 % over all
+    // cmd_bench poses at w = 64/96/128 against the unrestricted choice, and
+    // ahead of a per-pose line-count model, profiles/r02_sweep_orientation.txt)
     int r = 2;
     if (a.dim == 3) {
       double z[3] = {fabs(ps.mu[2][0]), fabs(ps.mu[2][1]), fabs(ps.mu[2][2])};
-      r = (z[0] <= z[1] && z[0] <= z[2]) ? 0 : (z[1] <= z[2] ? 1 : 2);
+      r = z[0] <= z[1] ? 0 : 1;
     }
     int o1 = (r + 1) % 3, o2 = (r + 2) % 3;
     if (a.dim == 2) { o1 = 0; o2 = 1; }
