@@ -260,7 +260,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     const double z0 = fabs(src[2] * a.rdom[0][2]), z1 = fabs(src[5] * a.rdom[1][2]),
                  z2 = fabs(src[8] * a.rdom[2][2]);  // |mu[2][b]|
     int r = 2;
-    if (a.dim == 3) r = (z0 <= z1 && z0 <= z2) ? 0 : (z1 <= z2 ? 1 : 2);
+    if (a.dim == 3) r = z0 <= z1 ? 0 : 1;  // never z: C1 loads along z runs scatter (cascade.cu)
     int o1 = (r + 1) % 3, o2 = (r + 2) % 3;
     if (a.dim == 2) { o1 = 0; o2 = 1; }
     const double zo1 = o1 == 0 ? z0 : (o1 == 1 ? z1 : z2), zo2 = o2 == 0 ? z0 : (o2 == 1 ? z1 : z2);
