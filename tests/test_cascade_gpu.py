@@ -124,6 +124,30 @@ def test_haptic_server_matches_one_shot(be):
             np.testing.assert_array_equal(g, w_)  # same kernel body, same reduction order
 
 
+def test_session_binding_operand_forms(be):
+    """The per-frame session call reads C-contiguous float64 R / t_eff in place
+    (csrc/pyfast.c); any other operand form (a transposed view, float32,
+    nested lists, a tuple) takes the ctypes path -- same bits either way."""
+    assert be._gf_fast is not None
+    rng = np.random.default_rng(31)
+    w = 32
+    C1, C2 = synthetic_window(rng, w), synthetic_window(rng, w)
+    W1, W2 = be.DeviceWindow(C1), be.DeviceWindow(C2)
+    dom, c = (0.09, 0.09, 0.09), (0.1, -0.2, 0.3)
+    R = random_rotation(rng)
+    t = rng.uniform(-1, 1, 3)
+    with be.HapticServer(W1, W2, False, dom, 0.5, c):
+        want = be.cascade(W1, W2, False, dom, 0.5, R, t, c)
+        forms = [(np.ascontiguousarray(R.T).T, t), (R.tolist(), tuple(t)), (R, list(t))]
+        for Rf, tf in forms:
+            got = be.cascade(W1, W2, False, dom, 0.5, Rf, tf, c)
+            np.testing.assert_array_equal(got, want)
+        t32 = t.astype(np.float32)  # float32 operand: the ctypes path widens it exactly
+        np.testing.assert_array_equal(be.cascade(W1, W2, False, dom, 0.5, R, t32, c),
+                                      be.cascade(W1, W2, False, dom, 0.5, R, t32.astype(np.float64), c))
+        assert be.cascade(W1, W2, False, dom, 0.5, R, t, c) is not be.cascade(W1, W2, False, dom, 0.5, R, t, c)
+
+
 def test_haptic_server_2d_fp64_and_idle_timeout(be):
     import time
 
