@@ -240,9 +240,9 @@ def test_cascade_3d_long_runs_launch_and_server(be, w, wrap, prec, tol):
 @pytest.mark.parametrize("w,prec", [(64, "fp32"), (32, "fp64"), (96, "fp32")])
 def test_serial_loop_matches_single_queries(be, w, prec):
     """gf_cascade_serial (one launch per pose, programmatic dependent launch:
-    query i+1 starts under query i's tail) gives every pose exactly the bits
-    of a lone gf_cascade call -- the overlapped queries share the partials
-    and ticket, which they touch only after the previous grid completed."""
+    up to three queries in flight) gives every pose exactly the bits of a lone
+    gf_cascade call -- the queries share a 4-slot scratch ring (partials,
+    ticket), each slot taken only after its previous user released it."""
     import torch
 
     rng = np.random.default_rng(70 + w)
@@ -256,6 +256,6 @@ def test_serial_loop_matches_single_queries(be, w, prec):
     out = be.cascade_batch(W1, W2, False, dom, dcell, c, poses, precision=prec, serial=True)
     torch.cuda.synchronize()
     got = out.cpu().numpy().view(np.complex128)
-    for i in list(range(0, n, 37)) + [n - 1]:
+    for i in range(n):  # every pose: the 4-slot scratch ring is reused 75 times per slot
         want = be.cascade(W1, W2, False, dom, dcell, Rs[i], ts[i], c, precision=prec)
         np.testing.assert_array_equal(got[i], want)
