@@ -9,7 +9,10 @@
 //     arguments), 32.32 fixed-point index coefficients, the lane orientation
 //     and -- for lattice-aligned poses -- the tie tables, all from the pose
 //     in one pass and one barrier;
-//   * mode loop: 2 x 148 CTAs of 256 threads; each CTA walks a contiguous
+//   * mode loop: 148 CTAs of 256 threads for a launch (two per SM for the
+//     resident server, cascade.cuh kLaunchCtasPerSm / kServerCtasPerSm);
+//     the serial loop chains launches by programmatic dependent launch over
+//     a 4-slot scratch ring (up to three queries in flight); each CTA walks a contiguous
 //     run of units (consecutive run-axis planes of one oriented 4 x 8 lane
 //     patch), so the fixed-point index advances by exact integer adds, the
 //     p/q phase product is reused and consecutive gathers reuse L1 lines;
