@@ -910,6 +910,14 @@ def stage_haptic(args, parity, cpu_ok, fp32_peak):
                         "misses": crun["deadline_misses"], "fields_done": done.get("fields"),
                         "fields_per_s": r4(done.get("fields", 0) / max(done.get("s", 1e-9), 1e-9)),
                         "server_sms": nsm * 3 // 4}
+    # the platform's own GPU-wide stalls in the same run: every SM spins on the
+    # clock for 5 s with no host interaction (gf_measure_stalls)
+    from paper_1711_05017_b200 import _lib
+
+    hb = np.zeros(4)
+    _lib.check(_lib.LIB.gf_measure_stalls(5.0, 500.0, _lib.dptr(hb)))
+    st["platform_stalls"] = {"seconds": 5.0, "max_gap_us": r4(hb[0]), "gaps_over_500us_per_sm": [int(hb[1]), int(hb[2])],
+                             "probe": "clock-only warp per SM, no host interaction"}
     if cpu_ok:
         C1h, C2h = np.asarray(W1), np.asarray(W2)
         c, dom, dcell = g.center(), g.delta_omega(), 1.0 / (g.node_count * g.cell_volume)

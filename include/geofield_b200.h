@@ -212,6 +212,12 @@ int gf_measure_launch(int n, int blocks, double *host_us, double *dev_us);
  * flag (cuStreamWaitValue32) p50 us, out[2] GPU read latency of mapped host
  * memory ns, out[3] mapped write + system fence ns. */
 int gf_measure_roundtrip(int n, double *out);
+/* GPU-wide stall detector: one warp per SM spins on %globaltimer for
+ * `seconds` (<= 60) with no host interaction.  out[0] longest gap between
+ * consecutive reads on any SM (us), out[1] / out[2] fewest / most gaps over
+ * threshold_us on one SM (equal counts on every SM: the whole GPU stopped),
+ * out[3] SMs watched. */
+int gf_measure_stalls(double seconds, double threshold_us, double *out);
 
 /* Persistent haptic server (Q1 latency path): a resident grid serves one
  * query per call through a host-mapped mailbox -- no kernel launch per

@@ -41,6 +41,7 @@ SIGNATURES = {
     "gf_measure_fma_peak": (ctypes.c_int, [ctypes.c_int, c_dp]),
     "gf_measure_roundtrip": (ctypes.c_int, [ctypes.c_int, c_dp]),
     "gf_measure_launch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_dp, c_dp]),
+    "gf_measure_stalls": (ctypes.c_int, [ctypes.c_double, ctypes.c_double, c_dp]),
     "gf_distance_winding": (ctypes.c_int, [ctypes.c_int, c_dp, ctypes.c_int64, c_dp, ctypes.c_int64, c_dp, c_dp]),
     "gf_sweep": (ctypes.c_int, [ctypes.c_int, c_dp, c_dp, c_dp, ctypes.c_int64, c_dp, c_dp, ctypes.c_int64,
                                 ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,

@@ -215,3 +215,61 @@ extern "C" int gf_measure_roundtrip(int n, double* out) {
   cudaStreamDestroy(st);
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// GPU-wide stall detector: one warp per SM spins on %globaltimer for a fixed
+// time with no host interaction and records, per SM, the longest gap between
+// consecutive reads and the number of gaps over a threshold.  A stall of the
+// whole GPU shows on every SM with the same count (the C5 frame misses).
+namespace gf {
+namespace {
+__global__ void heartbeat_kernel(unsigned long long dur_ns, unsigned long long thr_ns, unsigned long long* out) {
+  unsigned long long t0, t, prev, maxgap = 0, n = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  prev = t0;
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long g = t - prev;
+    maxgap = g > maxgap ? g : maxgap;
+    n += g > thr_ns;
+    prev = t;
+  } while (t - t0 < dur_ns);
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = maxgap;
+    out[2 * blockIdx.x + 1] = n;
+  }
+}
+}  // namespace
+}  // namespace gf
+
+// out[0]: longest gap (us) on any SM; out[1]/out[2]: fewest / most gaps over
+// threshold_us seen by one SM; out[3]: SMs watched
+extern "C" int gf_measure_stalls(double seconds, double threshold_us, double* out) {
+  using namespace gf;
+  GF_CHECK(out && seconds > 0 && seconds <= 60 && threshold_us > 0, GF_EINVAL, "bad argument");
+  const int sms = sm_count();
+  unsigned long long* d = nullptr;
+  GF_CUDA(cudaMalloc(&d, sizeof(unsigned long long) * 2 * sms));
+  cudaStream_t st;
+  GF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  heartbeat_kernel<<<sms, 32, 0, st>>>((unsigned long long)(seconds * 1e9), (unsigned long long)(threshold_us * 1e3),
+                                       d);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  std::vector<unsigned long long> h(2 * sms);
+  if (e == cudaSuccess) e = cudaMemcpy(h.data(), d, sizeof(unsigned long long) * 2 * sms, cudaMemcpyDeviceToHost);
+  cudaStreamDestroy(st);
+  cudaFree(d);
+  GF_CUDA(e);
+  unsigned long long mx = 0, nmin = ~0ull, nmax = 0;
+  for (int i = 0; i < sms; ++i) {
+    mx = std::max(mx, h[2 * i]);
+    nmin = std::min(nmin, h[2 * i + 1]);
+    nmax = std::max(nmax, h[2 * i + 1]);
+  }
+  out[0] = 1e-3 * (double)mx;
+  out[1] = (double)nmin;
+  out[2] = (double)nmax;
+  out[3] = (double)sms;
+  return 0;
+}
