@@ -47,6 +47,9 @@ struct SinglePose {
   double R[9];
   double targ[3];
   int p, q, r, nP, nQ;
+  // this CTA's unit range [u_begin, u_end) as (run, plane) of its first unit
+  // and the run as (p tile, q tile): one thread divides, the others read
+  int u_begin, u_end, run0, kr00, rp0, rq0;
   // finalize coefficients (computed during setup, used by the last block):
   double cg[3][3][3];  // G_g += cg[g][b][a] * Y[b][a]  (= -A_g[a][b] dw_a / dw_b)
   double kq[3][3];     // G_g += 2 pi i kq[g][a] Z_a     (= dw_a q_g[a])
@@ -273,6 +276,15 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
     sp.r = r;
     sp.nP = ((sp.p == 0 ? w0 : (sp.p == 1 ? w1 : w2)) + 15) / 16;
     sp.nQ = ((sp.q == 0 ? w0 : (sp.q == 1 ? w1 : w2)) + 15) / 16;
+    const int wr_ = r == 0 ? w0 : (r == 1 ? w1 : w2);
+    const int units_ = sp.nP * sp.nQ * wr_;
+    const int upb = (units_ + vg - 1) / vg;
+    sp.u_begin = min(units_, vb * upb);
+    sp.u_end = min(units_, sp.u_begin + upb);
+    sp.run0 = sp.u_begin / wr_;
+    sp.kr00 = sp.u_begin - sp.run0 * wr_;
+    sp.rp0 = sp.run0 / sp.nQ;
+    sp.rq0 = sp.run0 - sp.rp0 * sp.nQ;
   }
   if (tid == 192) {
     for (int ax = 0; ax < 3; ++ax) {
@@ -319,7 +331,6 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   const int lane = tid & 31, warp = tid >> 5;
   const int dp = 4 * (warp & 3) + (lane & 3);
   const int dq = 8 * (warp >> 2) + (lane >> 2);
-  const int units = sp.nP * sp.nQ * wr;
 
   Acc26<T> acc;
   acc.zero();
@@ -330,9 +341,7 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   // exact integer add per axis, C1 by one stride, and the seven per-mode
   // products go into 8 run sums (sum Y, sum j Y) folded into the 26 moments
   // once per segment -- the batched sweep's loop shape (cascade.cu).
-  const int upb = (units + vg - 1) / vg;
-  const int u_begin = vb * upb;
-  const int u_end = min(units, u_begin + upb);
+  const int u_begin = sp.u_begin, u_end = sp.u_end;
   const cx<T>* pt_p = ptab + (p == 0 ? 0 : (p == 1 ? w0 : w0 + w1));
   const cx<T>* pt_q = ptab + (q == 0 ? 0 : (q == 1 ? w0 : w0 + w1));
   const cx<T>* pt_r = ptab + (r == 0 ? 0 : (r == 1 ? w0 : w0 + w1));
@@ -349,11 +358,18 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   const int tmask = (sp.tie_dep[0] >= 0 ? 1 : 0) | (sp.tie_dep[1] >= 0 ? 2 : 0) | (a.dim == 3 && sp.tie_dep[2] >= 0 ? 4 : 0);
   const int sr = r == 0 ? w1 * w2 : (r == 1 ? w2 : 1);  // C1 stride along the run axis
   const T er0 = r == 0 ? (T)1 : (T)0, er1 = r == 1 ? (T)1 : (T)0, er2 = r == 2 ? (T)1 : (T)0;
+  // segment walk: (run, first plane) advance without divisions
+  int rp = sp.rp0, rq = sp.rq0, kr_first = sp.kr00;
   for (int seg = u_begin; seg < u_end;) {
-    const int run = seg / wr, kr0 = seg % wr;
+    const int kr0 = kr_first;
     const int kend = min(wr, kr0 + (u_end - seg));
     seg += kend - kr0;
-    const int kp = 16 * (run / sp.nQ) + dp, kq = 16 * (run % sp.nQ) + dq;
+    const int kp = 16 * rp + dp, kq = 16 * rq + dq;
+    kr_first = 0;  // the next segment starts a new run
+    if (++rq == sp.nQ) {
+      rq = 0;
+      ++rp;
+    }
     if (kp >= wp || kq >= wq) continue;
     const int kx0 = p == 0 ? kp : (q == 0 ? kq : kr0);
     const int ky0 = p == 1 ? kp : (q == 1 ? kq : kr0);
@@ -553,7 +569,8 @@ __device__ __forceinline__ void single_pose_body(const CascadeArgs& a, const dou
   unsigned crank, csize;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
-  const int cid = vb / (int)csize, nclusters = vg / (int)csize;
+  // (csize is kCluster, or 1 when the launch fell back to no clusters)
+  const int cid = csize == kCluster ? vb / kCluster : vb, nclusters = csize == kCluster ? vg / kCluster : vg;
   if (csize > 1) {
     if (cr.armed) {  // rank 0's barrier init is visible once the start barrier completes
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
