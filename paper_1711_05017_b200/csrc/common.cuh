@@ -119,7 +119,8 @@ constexpr unsigned kFixTieEps = 4295u;  // 1e-6 in units of 2^-32
 __device__ __forceinline__ int fix_floor(long long u) { return (int)(u >> 32); }
 __device__ __forceinline__ unsigned fix_lo(long long u) { return (unsigned)((unsigned long long)u & 0xffffffffull); }
 __device__ __forceinline__ float fix_frac(unsigned lo) { return __uint_as_float(0x3f800000u | (lo >> 9)) - 1.0f; }
-__device__ __forceinline__ bool fix_tie(unsigned lo) { return lo < kFixTieEps || lo > 0xffffffffu - kFixTieEps; }
+// lo < eps or lo > 2^32 - 1 - eps, as one wrapped compare
+__device__ __forceinline__ bool fix_tie(unsigned lo) { return lo + kFixTieEps < 2u * kFixTieEps; }
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
