@@ -878,7 +878,7 @@ def stage_haptic(args, parity, cpu_ok, fp32_peak):
               for m in run["missed"][:4]]
     st = {"frames": run["frames"], "p50_us": r4(run["p50_us"]), "p99_us": r4(run["p99_us"]),
           "max_us": r4(run["max_us"]), "misses": run["deadline_misses"], "missed": missed,
-          "miss_cause": "GPU-wide stall (gpu_clock_gap_us)",
+          "miss_cause": "GPU-wide stall (gpu_clock_gap_us)" if run["deadline_misses"] else None,
           "realtime": run["realtime"], "gpu_us_p50": r4(gpu_us),
           "roofline": {"bound": "fp32", "achieved": r4(achieved), "peak": r4(fp32_peak), "unit": "TFLOP/s",
                        "frac": r4(achieved / fp32_peak), "work": f"240 flop x live modes ({live:.3f} x {w5 ** 3})"},
