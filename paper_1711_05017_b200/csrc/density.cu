@@ -851,10 +851,21 @@ int gf_distance_winding(int d, const double* elems, int64_t ne, const double* P,
   src.P = (const double*)dp.p;
   src.d = d;
   unsigned grid = (unsigned)ceil_div(m, kThreads);
-  if (d == 3)
+  DevBuf dsorted, dspheres;
+  if (d == 3 && xi_out && !wind_out && m >= 256) {
+    // distances only, many points: the tile-culled kernel (same bits: the
+    // min is order-independent and the culling is conservative)
+    CullHost ch;
+    build_cull(elems, ne, ch);
+    CullInfo ci;
+    if ((rc = upload_cull(ch, ne, 0, dsorted, dspheres, ci, st))) return rc;
+    dist_wind_culled_kernel<<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, ci, (double*)dx.p, nullptr);
+    GF_CUDA(cudaStreamSynchronize(st));  // `ch` leaves scope
+  } else if (d == 3) {
     dist_wind_kernel<3><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dx.p, (double*)dw.p);
-  else
+  } else {
     dist_wind_kernel<2><<<grid, kThreads, 0, st>>>(src, (const double*)de.p, ne, m, (double*)dx.p, (double*)dw.p);
+  }
   GF_CUDA(cudaGetLastError());
   if (xi_out) GF_CUDA(cudaMemcpyAsync(xi_out, dx.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
   if (wind_out) GF_CUDA(cudaMemcpyAsync(wind_out, dw.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));

@@ -31,6 +31,21 @@ def test_distance_and_winding_bitwise():
         np.testing.assert_array_equal(w_gpu >= 0.5, w_cpu >= 0.5)
 
 
+def test_distance_culled_on_thread_mesh_bitwise():
+    """Large distance batches take the tile-culled kernel (Morton tiles,
+    vertex upper bound, running minimum): on the ~10^5-face nut, points on and
+    just off the surface and far away give the brute-force minimum exactly."""
+    rng = np.random.default_rng(7)
+    solid = scenes.get_scene("bolt_nut").fixed
+    elems = solid.element_arrays()[0]
+    verts = elems.reshape(-1, 3)
+    near = verts[rng.integers(0, len(verts), 3000)] + rng.normal(scale=1e-3, size=(3000, 3))
+    on = verts[rng.integers(0, len(verts), 500)]  # exactly on the surface: distance 0
+    far = rng.uniform(-2.0, 2.0, size=(1500, 3))
+    P = np.concatenate([near, on, far])
+    np.testing.assert_array_equal(backend.distance_batch(solid, P), oracle.distance(elems, P))
+
+
 def test_sweep_decisions_bitwise_values_tight():
     rng = np.random.default_rng(2)
     for solid in (scenes.icosphere(0.4, 2), scenes.random_polygon(rng, 9)):
