@@ -70,8 +70,11 @@ __device__ __forceinline__ double exact_u_f(const double* R, const double* dom, 
 // the mode axis with the largest component along C2's contiguous axis.  The
 // gathered V * phase goes through shared memory and the C1 read and Q write
 // are done in z-fastest order, coalesced.  fp32 indices in 32.32 fixed point.
+// fp32: at most 51 registers so five CTAs (40 warps) share an SM -- the
+// gathers are latency bound: 3.33 -> 3.16 ms for the 512^3 landscape against
+// the default four (profiles/r02_product_occupancy.txt)
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(256) product_brick_kernel(RotArgs a) {
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) product_brick_kernel(RotArgs a) {
   using P4 = typename pair4<T>::type;
   __shared__ cx<T> sq[8 * 73];
   __shared__ cx<T> ph[3][8];  // exp(2 pi i dw_a s_a (k_a - h_a)) for this brick's 8 modes per axis
