@@ -146,8 +146,12 @@ struct Orient {
   double step_re[3], step_im[3];
 };
 
+// fp32: four resident CTAs per SM (64 registers; the spilled values are
+// per-pose constants, L1-resident): the L2-resident gathers are latency
+// bound, and twice the warps gain 14-15 % poses/s at w = 64-128 over two CTAs
+// (five or more collapse under spills; profiles/r02_sweep_orientation.txt)
 template <typename T, bool WRAP>
-__global__ void __launch_bounds__(kThreads) cascade3d_kernel(CascadeArgs a) {
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2) cascade3d_kernel(CascadeArgs a) {
   using P4 = typename pair4<T>::type;
   __shared__ PoseShared ps;
   __shared__ Orient orient;
