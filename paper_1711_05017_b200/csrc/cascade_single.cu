@@ -66,11 +66,12 @@ constexpr int kMaxCluster = 8;
 static_assert(kCluster <= kMaxCluster, "cluster stage sized for kMaxCluster ranks");
 // resident CTAs per SM the register budget is sized for: the server grid is
 // kServerCtasPerSm x 148 CTAs (up to 128 registers); the one-shot kernel runs
-// kLaunchCtasPerSm per SM and keeps room for three (<= 80 registers), so the
-// CTAs of the next two launches of a PDL chain start beside the previous
-// tail (cascade.cuh)
+// kLaunchCtasPerSm per SM and keeps room for four (64 registers), so the CTAs
+// of the next launches of a PDL chain start beside the previous tail
+// (cascade.cuh; serial loop w = 64: 4.46 -> 4.31 us/query against room for
+// three, the lone launch ~3 % slower -- profiles/r02_cascade_grid.txt)
 constexpr int kMinBlocksServer = kServerCtasPerSm;
-constexpr int kMinBlocksLaunch = 3;
+constexpr int kMinBlocksLaunch = 4;
 struct ClusterRed {
   double gather[kMaxCluster][kNumMoments];
   unsigned long long bar;
