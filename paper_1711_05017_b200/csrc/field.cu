@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) product_brick_ker
   __shared__ cx<T> tt[3][8];  // lattice-aligned poses: (floor, frac) of u_c at this brick's k_b, b = tie_dep[c]
   const int w0 = a.w[0], w1 = a.w[1], w2 = a.w[2];
   const int hx = w0 / 2, hy = w1 / 2, hz = w2 / 2;
-  const int nbz = (w2 + 7) / 8, nby = (w1 + 7) / 8;
-  const int bz = blockIdx.x % nbz, by = (blockIdx.x / nbz) % nby, bx = blockIdx.x / (nbz * nby);
+  // brick (bx, by, bz) straight from a 3-D grid (z fastest): no index divisions
+  const int bz = blockIdx.x, by = blockIdx.y, bx = blockIdx.z;
   const int t = threadIdx.x;
   const int sy = w2 + 1, sx = (w1 + 2) * (w2 + 1);
   const P4* __restrict__ C2 = reinterpret_cast<const P4*>(a.C2p);
@@ -113,13 +113,17 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) product_brick_ker
   }
   __syncthreads();
   // C1 for the epilogue's (z-fastest) modes, issued before the gathers
+  // brick origin in the (kx0-offset) C1 / output arrays, then 32-bit offsets
+  const int64_t brick0 = ((int64_t)(bx * 8) * w1 + by * 8) * w2 + bz * 8;
+  const int64_t c1brick0 = brick0 + (int64_t)a.kx0 * w1 * w2;
+  const int plane = w1 * w2;
   cx<T> c1v[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int oz = t & 7, oy = (t >> 3) & 7, ox = (t >> 6) + 4 * h;
     const int kxl = bx * 8 + ox, ky = by * 8 + oy, kz = bz * 8 + oz;
     c1v[h] = mk<T>(1, 0);
-    if (a.C1 && kxl < a.nkx && ky < w1 && kz < w2) c1v[h] = C1[((int64_t)(a.kx0 + kxl) * w1 + ky) * w2 + kz];
+    if (a.C1 && kxl < a.nkx && ky < w1 && kz < w2) c1v[h] = C1[c1brick0 + (ox * plane + oy * w2 + oz)];
   }
   // fp32 indices: the 32.32 fixed-point u of this thread's first mode, the
   // second (4 further along the slowest lane axis) by one exact 64-bit add
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 5 : 4) product_brick_ker
     const int kxl = bx * 8 + ox, ky = by * 8 + oy, kz = bz * 8 + oz;
     if (kxl >= a.nkx || ky >= w1 || kz >= w2) continue;
     const cx<T> q = c1v[h] * sq[ox * 73 + oy * 9 + oz];
-    out[((int64_t)kxl * w1 + ky) * w2 + kz] = q;
+    out[brick0 + (ox * plane + oy * w2 + oz)] = q;
   }
 }
 
@@ -287,7 +291,8 @@ int gf_rotate_product_planes(uint64_t h1, uint64_t h2, int wrap, const double* d
     a.perm[1] = pm;
     a.perm[2] = 3 - pf - pm;
   }
-  const unsigned bricks = (unsigned)(ceil_div(a.nkx, 8) * ceil_div(a.w[1], 8) * ceil_div(a.w[2], 8));
+  const dim3 bricks((unsigned)ceil_div(a.w[2], 8), (unsigned)ceil_div(a.w[1], 8), (unsigned)ceil_div(a.nkx, 8));
+  GF_CHECK(bricks.y <= 65535 && bricks.z <= 65535, GF_EINVAL, "window too large for the brick grid");
   if (precision == 32) {
     if (wrap) product_brick_kernel<float, true><<<bricks, 256, 0, st>>>(a);
     else product_brick_kernel<float, false><<<bricks, 256, 0, st>>>(a);
