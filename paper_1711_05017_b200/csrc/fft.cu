@@ -175,6 +175,13 @@ __device__ __forceinline__ void store_line(const FftArgs& a, const LineAddr& L, 
   cx<T>* __restrict__ out = reinterpret_cast<cx<T>*>(a.out);
   const int Lout = a.shape_out[a.axis], hout = Lout / 2;
   if (!L.live) return;
+  if (!a.out_centered && !a.out_phase_kind && a.scale == 1.0 && L.st_out == 1) {
+    // node-order output of a contiguous line, no scale or phase: a plain copy
+    cx<T>* __restrict__ o = out + L.base_out;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) o[j + r * TPL] = line[sidx<T>(j + r * TPL)];
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int pos = j + r * TPL;
@@ -362,6 +369,18 @@ __global__ void __launch_bounds__((128 / sizeof(cx<T>)) * (N / 8))
     if (blockIdx.x + gridDim.x < ntiles) issue_load(blockIdx.x + gridDim.x, 1);
   }
   __syncthreads();
+  // this thread's input rows (the same for every tile): source row or -1
+  int srow[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int pos = j + r * TPL;
+    if (a.in_centered) {
+      const int m = pos < N / 2 ? pos : pos - N;
+      srow[r] = (m + hin < 0 || m + hin >= Lin) ? -1 : (m + hin) * RB + b;
+    } else {
+      srow[r] = pos * RB + b;
+    }
+  }
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int s = it % 3;
@@ -369,23 +388,14 @@ __global__ void __launch_bounds__((128 / sizeof(cx<T>)) * (N / 8))
     mbar_wait(&bars[s], (it / 3) & 1);
     cx<T> v[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int pos = j + r * TPL;
-      int src, m;
-      if (a.in_centered) {
-        m = pos < N / 2 ? pos : pos - N;
-        src = m + hin;
-        if (src < 0 || src >= Lin) src = -1;
-      } else {
-        m = pos;
-        src = pos;
+    for (int r = 0; r < 8; ++r) v[r] = srow[r] >= 0 ? buf[srow[r]] : mk<T>(0, 0);
+    if (a.in_phase_kind) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int pos = j + r * TPL;
+        const int m = a.in_centered ? (pos < N / 2 ? pos : pos - N) : pos;
+        if (srow[r] >= 0) v[r] = v[r] * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
       }
-      cx<T> x = mk<T>(0, 0);
-      if (src >= 0) {
-        x = buf[src * RB + b];
-        if (a.in_phase_kind) x = x * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
-      }
-      v[r] = x;
     }
     fft_line<T, N, RB>(v, buf + b, j, tw, a.sign);  // ends with __syncthreads
     if (a.scale != 1.0 || a.out_phase_kind) {
