@@ -264,6 +264,18 @@ __global__ void __launch_bounds__(B * (N / 8)) fft_rows_staged_kernel(FftArgs a,
   }
   cx<T>* line = lines + b * LD;
   const int hin = Lin / 2;
+  // this thread's source positions in its line (the same for every tile), -1: zero
+  int spos[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int pos = j + r * TPL;
+    if (a.in_centered) {
+      const int m = pos < N / 2 ? pos : pos - N;
+      spos[r] = (m + hin < 0 || m + hin >= Lin) ? -1 : m + hin;
+    } else {
+      spos[r] = pos < Lin ? pos : -1;
+    }
+  }
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int s = it & 1;
@@ -272,23 +284,14 @@ __global__ void __launch_bounds__(B * (N / 8)) fft_rows_staged_kernel(FftArgs a,
     const cx<T>* src_line = stage0 + s * tile_elems + b * Lin;
     cx<T> v[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int pos = j + r * TPL;
-      int src, m;
-      if (a.in_centered) {
-        m = pos < N / 2 ? pos : pos - N;
-        src = m + hin;
-        if (src < 0 || src >= Lin) src = -1;
-      } else {
-        m = pos;
-        src = pos;
+    for (int r = 0; r < 8; ++r) v[r] = (L.live && spos[r] >= 0) ? src_line[spos[r]] : mk<T>(0, 0);
+    if (a.in_phase_kind) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int pos = j + r * TPL;
+        const int m = a.in_centered ? (pos < N / 2 ? pos : pos - N) : pos;
+        if (L.live && spos[r] >= 0) v[r] = v[r] * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
       }
-      cx<T> x = mk<T>(0, 0);
-      if (L.live && src >= 0) {
-        x = src_line[src];
-        if (a.in_phase_kind) x = x * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
-      }
-      v[r] = x;
     }
     __syncthreads();  // stage s fully read: refill it two tiles ahead
     if (tid == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, s);
