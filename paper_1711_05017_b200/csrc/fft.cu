@@ -400,8 +400,13 @@ __global__ void __launch_bounds__((128 / sizeof(cx<T>)) * (N / 8))
         if (srow[r] >= 0) v[r] = v[r] * phase_factor<T>(a.in_phase_kind, a.in_phase, m);
       }
     }
+    if (a.scale != 1.0 && !a.out_phase_kind) {  // linear: scale the inputs, no extra pass over the tile
+      const T sc = (T)a.scale;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = mk<T>(v[r].re * sc, v[r].im * sc);
+    }
     fft_line<T, N, RB>(v, buf + b, j, tw, a.sign);  // ends with __syncthreads
-    if (a.scale != 1.0 || a.out_phase_kind) {
+    if (a.out_phase_kind) {
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int pos = j + r * TPL;
