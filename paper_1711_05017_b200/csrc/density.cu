@@ -4,8 +4,10 @@
 // separately rounded, exactly as the reference's plain -O3 x86-64 build of
 // _core.pyx, so point-element distances, exclusion (xi < eta_floor h),
 // subdivision decisions, residual flags and occupancy reproduce the
-// reference bit for bit.  (Values that go through exp/atan2 agree to libm
-// ulps, well inside 1e-9.)
+// reference bit for bit.  Values agree to a few ulps, well inside the 1e-12
+// the tests use: exp/atan2 differ from libm by ulps, and the 3D sweep leaf
+// regroups its divisions and uses exp2 and explicit FMAs (sweep_kernel); no
+// decision is taken on a regrouped quantity.
 //
 // Reference kernels (/root/reference/pkg/src/geofield/_core.pyx):
 //   distance   _tri_dist_3d 65-99, distance_3d 189-230 (BVH; here a brute
